@@ -1,0 +1,192 @@
+/*
+ * ktune_b200.h -- the C-ABI drop-in boundary of the B200 build of ISAAC's
+ * GEMM/CONV tuning path (paper_1802_05371_b200/libktune_b200.so).
+ *
+ * The reference (ktune, /root/reference/proj) is a C++20 library with no FFI
+ * of its own; a C++ host that wants its GEMM/CONV path on the GPU crosses to
+ * the device exactly where the reference calls its executors and its
+ * measurement backend.  Every entry point below names the reference
+ * interface it replaces (file:line under /root/reference/proj).  The C++
+ * adapter a maintainer would add (a MeasurementBackend subclass and a
+ * ctypes binding) is shown in INTEGRATION.md.
+ *
+ * Conventions
+ *  - plain C types only; structs mirror the reference types field-for-field
+ *    in canonical order (param_space.hpp:20-106);
+ *  - every function returns a ktune_status; on failure ktune_last_error()
+ *    returns a thread-local message (the reference's exception what());
+ *  - "device" pointers are CUDA device pointers owned by the caller, and
+ *    `stream` is a cudaStream_t (NULL = legacy default stream);
+ *  - no CPU fallback: if the CUDA kernels cannot run, calls fail with
+ *    KTUNE_ERR_CUDA.
+ */
+#ifndef KTUNE_B200_H
+#define KTUNE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define KTUNE_API __attribute__((visibility("default")))
+#else
+#define KTUNE_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KTUNE_B200_ABI_VERSION 1
+
+/* Error classes of the reference, as codes (backends.cpp:120-125, 220-240,
+ * 504-506; pipeline.cpp runtime_error paths). */
+typedef enum ktune_status {
+    KTUNE_OK = 0,
+    KTUNE_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument: illegal tuning, size mismatch, bad field */
+    KTUNE_ERR_UNSUPPORTED = 2,      /* dtype/tuple this build cannot execute ("cpu backend does not execute f16") */
+    KTUNE_ERR_CUDA = 3,             /* a CUDA call failed */
+    KTUNE_ERR_RUNTIME = 4,          /* std::runtime_error: malformed file, IO */
+    KTUNE_ERR_WORKSPACE = 5         /* caller workspace smaller than *_workspace_size() */
+} ktune_status;
+
+/* Dtype of param_space.hpp:15 (f16/f32/f64) plus the tensor-core extensions. */
+typedef enum ktune_dtype {
+    KTUNE_F16 = 0,
+    KTUNE_F32 = 1,
+    KTUNE_F64 = 2,
+    KTUNE_BF16 = 3,
+    KTUNE_TF32 = 4
+} ktune_dtype;
+
+/* FAST: FFMA (SIMT) / tensor cores.  PARITY: bit-identical to the reference
+ * executors execute_gemm<T>/execute_conv<T> (f32/f64 only). */
+typedef enum ktune_mode { KTUNE_MODE_FAST = 0, KTUNE_MODE_PARITY = 1 } ktune_mode;
+
+/* GemmInput, param_space.hpp:20-30. */
+typedef struct ktune_gemm_input {
+    int64_t m, n, k;
+    int32_t dtype; /* ktune_dtype */
+    int32_t trans_a;
+    int32_t trans_b;
+    int32_t reserved;
+} ktune_gemm_input;
+
+/* ConvInput, param_space.hpp:34-49 (valid mode: H = P+R-1, W = Q+S-1). */
+typedef struct ktune_conv_input {
+    int64_t n_batch, p, q, k_filters, c, r, s;
+    int32_t dtype;
+    int32_t reserved;
+} ktune_conv_input;
+
+/* GemmTuning, param_space.hpp:55-67 (canonical order m_s n_s m_l n_l u k_s k_l k_g). */
+typedef struct ktune_gemm_tuning {
+    int32_t m_s, n_s, m_l, n_l, u, k_s, k_l, k_g;
+} ktune_gemm_tuning;
+
+/* ConvTuning, param_space.hpp:69-77. */
+typedef struct ktune_conv_tuning {
+    int32_t k_s, p_s, q_s, n_s, k_l, p_l, q_l, n_l, u, c_s, c_l, c_g;
+} ktune_conv_tuning;
+
+/* HardwareDescriptor, param_space.hpp:87-106. */
+typedef struct ktune_hw {
+    int64_t max_shared_bytes_per_block;
+    int64_t max_registers_per_thread;
+    int64_t max_threads_per_block;
+    int64_t max_warps_per_multiprocessor;
+    int64_t warp_size;
+    double alu_latency, alu_throughput, mem_latency, mem_throughput, clock_hz;
+    int64_t num_multiprocessors;
+} ktune_hw;
+
+/* ResourceUsage, param_space.hpp:108-114. */
+typedef struct ktune_resources {
+    int64_t shared_bytes, registers_per_thread, threads_per_block;
+} ktune_resources;
+
+/* Options of a device measurement (CpuBackend ctor, backends.hpp:128-137,
+ * plus the device-timing knobs the reference does not need). */
+typedef struct ktune_measure_options {
+    int32_t mode;        /* ktune_mode */
+    int32_t repetitions; /* timed runs, best-of (reference default 3) */
+    int32_t warmup;      /* untimed runs first (reference: 1) */
+    int32_t flush_l2;    /* write-sweep L2 before each timed run */
+    uint64_t seed;       /* operand fill seed (reference: 0x5eed) */
+} ktune_measure_options;
+
+/* ---- library ------------------------------------------------------------ */
+KTUNE_API int ktune_abi_version(void);
+KTUNE_API const char* ktune_last_error(void);
+/* Selects the CUDA device used by subsequent host-buffer / measurement calls. */
+KTUNE_API int ktune_set_device(int device);
+
+/* ---- parameter space (param_space.cpp) ----------------------------------- */
+/* HardwareDescriptor::from_json_text / defaults (param_space.cpp:140-178). */
+KTUNE_API int ktune_hw_default(ktune_hw* out);
+KTUNE_API int ktune_hw_from_json(const char* json_text, ktune_hw* out);
+/* estimate_resources (param_space.cpp:204-231). */
+KTUNE_API int ktune_estimate_resources_gemm(const ktune_gemm_input* in, const ktune_gemm_tuning* t, ktune_resources* out);
+KTUNE_API int ktune_estimate_resources_conv(const ktune_conv_input* in, const ktune_conv_tuning* t, ktune_resources* out);
+/* is_legal (param_space.cpp:275-314): *accepted 0/1, *reason = RejectReason
+ * (0 divisibility, 1 shared_memory, 2 registers, 3 threads); detail text via
+ * ktune_last_text(). */
+KTUNE_API int ktune_is_legal_gemm(const ktune_hw* hw, const ktune_gemm_input* in, const ktune_gemm_tuning* t, int* accepted,
+                        int* reason);
+KTUNE_API int ktune_is_legal_conv(const ktune_hw* hw, const ktune_conv_input* in, const ktune_conv_tuning* t, int* accepted,
+                        int* reason);
+KTUNE_API const char* ktune_last_text(void);
+/* enumerate_legal (param_space.cpp:536-628); bounds_json NULL/"" = defaults
+ * (powers of two 1..16).  Writes min(count, cap) tunings; *count = total. */
+KTUNE_API int ktune_enumerate_legal_gemm(const ktune_hw* hw, const ktune_gemm_input* in, const char* bounds_json,
+                               ktune_gemm_tuning* out, int64_t cap, int64_t* count);
+KTUNE_API int ktune_enumerate_legal_conv(const ktune_hw* hw, const ktune_conv_input* in, const char* bounds_json,
+                               ktune_conv_tuning* out, int64_t cap, int64_t* count);
+/* encode_features gemm.v1 (14) / conv.v1 (19) (param_space.cpp:630-659). */
+KTUNE_API int ktune_encode_features_gemm(const ktune_gemm_input* in, const ktune_gemm_tuning* t, double* out14);
+KTUNE_API int ktune_encode_features_conv(const ktune_conv_input* in, const ktune_conv_tuning* t, double* out19);
+/* build_indirection_table (backends.cpp:197-216): 4 int64 per entry
+ * {c, r, s, image_offset}; cap in entries, *count = C*R*S. */
+KTUNE_API int ktune_build_indirection_table(const ktune_conv_input* in, int64_t* out4, int64_t cap, int64_t* count);
+
+/* ---- device kernels (replace execute_gemm / execute_conv, backends.cpp:228-444) */
+/* Workspace for k_g / c_g partials; zero-fill it once before first use
+ * (per-tile arrival counters live at its head and are left zeroed). */
+KTUNE_API int ktune_gemm_workspace_size(const ktune_gemm_input* in, const ktune_gemm_tuning* t, size_t* bytes);
+KTUNE_API int ktune_conv_workspace_size(const ktune_conv_input* in, const ktune_conv_tuning* t, size_t* bytes);
+/* C = op(A) op(B) on device buffers (row-major; A M x K or K x M when
+ * trans_a; B K x N or N x K when trans_b; C M x N).  f32/f64: SIMT family
+ * (mode selects FAST or PARITY).  bf16/f16/tf32: tcgen05 family, fp32 C. */
+KTUNE_API int ktune_gemm(const ktune_gemm_input* in, const ktune_gemm_tuning* t, int mode, const void* a, const void* b,
+               void* c, void* workspace, size_t workspace_bytes, void* stream);
+/* Valid-mode implicit-GEMM convolution: images C,H,W,N; filters C,R,S,K;
+ * outputs K,P,Q,N. */
+KTUNE_API int ktune_conv(const ktune_conv_input* in, const ktune_conv_tuning* t, int mode, const void* images,
+               const void* filters, void* outputs, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Host-buffer drop-ins with the executor's own contract: element counts are
+ * checked like the spans of backends.cpp:237-240 ("operand size mismatch");
+ * inputs are copied to the device, the kernel runs, the result is copied back
+ * before return. */
+KTUNE_API int ktune_execute_gemm(const ktune_gemm_input* in, const ktune_gemm_tuning* t, int mode, const void* a, int64_t a_len,
+                       const void* b, int64_t b_len, void* c, int64_t c_len);
+KTUNE_API int ktune_execute_conv(const ktune_conv_input* in, const ktune_conv_tuning* t, int mode, const void* images,
+                       int64_t images_len, const void* filters, int64_t filters_len, void* outputs,
+                       int64_t outputs_len);
+
+/* ---- measurement (replaces CpuBackend::measure, backends.cpp:502-556) ---- */
+/* require_legal under hw, seeded device operands, warm-up, best-of
+ * repetitions timed with CUDA events (L2 flushed before each), returns
+ * GFLOPS = 2MNK / best / 1e9 (CONV 2NPQKCRS).  opts NULL = defaults
+ * {FAST, 3, 1, 1, 0x5eed}. */
+KTUNE_API int ktune_measure_gemm(const ktune_hw* hw, const ktune_gemm_input* in, const ktune_gemm_tuning* t,
+                       const ktune_measure_options* opts, double* gflops);
+KTUNE_API int ktune_measure_conv(const ktune_hw* hw, const ktune_conv_input* in, const ktune_conv_tuning* t,
+                       const ktune_measure_options* opts, double* gflops);
+/* Evicts L2 with a write sweep larger than the cache (K8). */
+KTUNE_API int ktune_l2_flush(void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KTUNE_B200_H */

@@ -1,0 +1,18 @@
+// simt_gemm_f32_fast.cu -- ahead-of-time instantiations of the SIMT family:
+// gemm, float, FFMA fast mode.  See simt.cuh / simt_tiles.cuh.
+#include "simt.cuh"
+#include "simt_tiles.cuh"
+
+namespace ktune_dev {
+
+#define CASE(A, B, C) \
+    if (ms == A && ns == B && ks == C) return reinterpret_cast<const void*>(&simt_kernel<GemmProblem<float>, float, A, B, C, false>);
+
+const void* simt_gemm_f32_fast(int ms, int ns, int ks) {
+    if (ms == 0 && ns == 0 && ks == 0)
+        return reinterpret_cast<const void*>(&simt_kernel<GemmProblem<float>, float, 0, 0, 0, false>);
+    KTUNE_GEMM_TILES(CASE)
+    return nullptr;
+}
+
+}  // namespace ktune_dev

@@ -1,0 +1,46 @@
+// simt_tiles.cuh -- the register-tile envelope compiled ahead of time.
+//
+// GEMM (MS=m_s, NS=n_s, KS=k_s): MS,NS in {1,2,4,8}, KS in {1,2,4},
+//   MS*NS*KS <= 128.  CONV (MS=k_s, NS=p_s*q_s*n_s, KS=c_s): MS in {1,2,4,8},
+//   NS in {1,2,4,8,16}, KS in {1,2}, product <= 128.  Everything outside runs
+//   on the runtime-tile generic instantiation (MS=NS=KS=0).
+#pragma once
+
+#define KTUNE_GEMM_TILES_KS(X, KS) \
+    X(1, 1, KS) X(1, 2, KS) X(2, 1, KS) X(1, 4, KS) X(2, 2, KS) X(4, 1, KS) X(1, 8, KS) X(2, 4, KS) X(4, 2, KS) \
+    X(8, 1, KS) X(2, 8, KS) X(4, 4, KS) X(8, 2, KS) X(4, 8, KS) X(8, 4, KS)
+
+#define KTUNE_GEMM_TILES(X) \
+    KTUNE_GEMM_TILES_KS(X, 1) KTUNE_GEMM_TILES_KS(X, 2) KTUNE_GEMM_TILES_KS(X, 4) X(8, 8, 1) X(8, 8, 2)
+
+#define KTUNE_CONV_TILES_CS(X, CS) \
+    X(1, 1, CS) X(1, 2, CS) X(1, 4, CS) X(1, 8, CS) X(1, 16, CS) \
+    X(2, 1, CS) X(2, 2, CS) X(2, 4, CS) X(2, 8, CS) X(2, 16, CS) \
+    X(4, 1, CS) X(4, 2, CS) X(4, 4, CS) X(4, 8, CS) X(4, 16, CS) \
+    X(8, 1, CS) X(8, 2, CS) X(8, 4, CS) X(8, 8, CS)
+
+#define KTUNE_CONV_TILES(X) KTUNE_CONV_TILES_CS(X, 1) X(8, 16, 1) KTUNE_CONV_TILES_CS(X, 2)
+
+namespace ktune_dev {
+
+// Kernel pointer lookup per (kind, dtype, mode); defined in
+// simt_<kind>_<T>_<mode>.cu.  Returns nullptr for tiles outside the envelope;
+// (0,0,0) is the generic runtime-tile instantiation.
+#define KTUNE_DECLARE_LOOKUP(KIND, T, MODE) const void* simt_##KIND##_##T##_##MODE(int ms, int ns, int ks);
+KTUNE_DECLARE_LOOKUP(gemm, f32, parity)
+KTUNE_DECLARE_LOOKUP(gemm, f32, fast)
+KTUNE_DECLARE_LOOKUP(gemm, f64, parity)
+KTUNE_DECLARE_LOOKUP(gemm, f64, fast)
+KTUNE_DECLARE_LOOKUP(conv, f32, parity)
+KTUNE_DECLARE_LOOKUP(conv, f32, fast)
+KTUNE_DECLARE_LOOKUP(conv, f64, parity)
+KTUNE_DECLARE_LOOKUP(conv, f64, fast)
+
+// Max threads the (ms,ns,ks) instantiation was compiled for.
+inline int simt_thread_cap(int ms, int ns, int ks) {
+    if (ms == 0) return 1024;
+    const int acc = ms * ns * ks;
+    return acc <= 16 ? 1024 : (acc <= 64 ? 512 : 256);
+}
+
+}  // namespace ktune_dev
