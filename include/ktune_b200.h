@@ -149,8 +149,9 @@ KTUNE_API int ktune_encode_features_conv(const ktune_conv_input* in, const ktune
 KTUNE_API int ktune_build_indirection_table(const ktune_conv_input* in, int64_t* out4, int64_t cap, int64_t* count);
 
 /* ---- device kernels (replace execute_gemm / execute_conv, backends.cpp:228-444) */
-/* Workspace for k_g / c_g partials; zero-fill it once before first use
- * (per-tile arrival counters live at its head and are left zeroed). */
+/* Workspace for k_g / c_g partials (0 bytes when the reduction is not split
+ * across the grid).  No initialisation is needed: publication flags carry a
+ * token unique to each launch.  One launch at a time per workspace. */
 KTUNE_API int ktune_gemm_workspace_size(const ktune_gemm_input* in, const ktune_gemm_tuning* t, size_t* bytes);
 KTUNE_API int ktune_conv_workspace_size(const ktune_conv_input* in, const ktune_conv_tuning* t, size_t* bytes);
 /* C = op(A) op(B) on device buffers (row-major; A M x K or K x M when

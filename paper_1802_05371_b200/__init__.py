@@ -293,14 +293,14 @@ _workspaces: dict = {}
 
 
 def _workspace(device, nbytes: int):
-    """Grow-only zero-initialised workspace per device (counters must start at 0)."""
+    """Grow-only workspace per device (no initialisation needed)."""
     import torch
     if nbytes == 0:
         return None, 0
     key = torch.device(device).index
     ws = _workspaces.get(key)
     if ws is None or ws.numel() < nbytes:
-        ws = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
         _workspaces[key] = ws
     return ws, ws.numel()
 

@@ -40,9 +40,10 @@ enum class Mode : int {
 };
 
 // Bytes of workspace a launch needs (0 when k_g splits collapse to one
-// slice).  The first 256-byte-aligned region holds per-tile arrival
-// counters that must be zero before the first launch; every launch leaves
-// them zero again, so a workspace is zero-filled once and then reused.
+// slice): per-(slice, tile) publication flags followed by the partial tiles
+// of slices 0..nz-2.  Flags carry a token unique to each launch, so the
+// workspace needs no initialisation and can be reused freely (one launch at a
+// time per workspace).
 std::size_t gemm_workspace_bytes(const GemmInput& in, const GemmTuning& t);
 std::size_t conv_workspace_bytes(const ConvInput& in, const ConvTuning& t);
 

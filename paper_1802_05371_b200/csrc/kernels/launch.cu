@@ -11,6 +11,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <random>
 #include <cstdio>
 #include <mutex>
 #include <string>
@@ -102,8 +105,10 @@ Plan plan_simt(std::int64_t rows, std::int64_t red, std::int64_t out_elems, std:
     pl.ns = ns;
     pl.ks = ks;
     if (p.nz > 1) {
-        pl.counter_bytes = (std::size_t(pl.col_tiles) * pl.row_tiles * sizeof(unsigned) + 255) / 256 * 256;
-        pl.ws_bytes = pl.counter_bytes + std::size_t(p.nz) * std::size_t(out_elems) * std::size_t(esize);
+        pl.counter_bytes =
+            (std::size_t(pl.col_tiles) * pl.row_tiles * std::size_t(p.nz - 1) * sizeof(unsigned long long) + 255) /
+            256 * 256;
+        pl.ws_bytes = pl.counter_bytes + std::size_t(p.nz - 1) * std::size_t(out_elems) * std::size_t(esize);
     }
     return pl;
 }
@@ -141,13 +146,29 @@ void prepare(const void* kernel, std::size_t smem) {
     configured[kernel] = std::max<std::size_t>(smem, 48 * 1024);
 }
 
+// Launch tokens: a process-random salt mixed with a counter (never 0).
+unsigned long long next_token() {
+    static std::atomic<unsigned long long> counter{0};
+    static const unsigned long long salt = [] {
+        std::random_device rd;
+        return (static_cast<unsigned long long>(rd()) << 32) ^ rd() ^
+               static_cast<unsigned long long>(std::chrono::steady_clock::now().time_since_epoch().count());
+    }();
+    unsigned long long x = salt + 0x9e3779b97f4a7c15ULL * (counter.fetch_add(1) + 1);
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    x ^= x >> 31;
+    return x == 0 ? 1 : x;
+}
+
 void bind_workspace(Plan& pl, void* ws, std::size_t ws_bytes) {
     if (pl.p.nz <= 1) return;
     if (ws == nullptr || ws_bytes < pl.ws_bytes)
         throw workspace_error("workspace of " + std::to_string(ws_bytes) + " bytes is smaller than the " +
                               std::to_string(pl.ws_bytes) + " bytes this tuning needs");
-    pl.p.counters = static_cast<unsigned*>(ws);
+    pl.p.flags = static_cast<unsigned long long*>(ws);
     pl.p.ws = static_cast<unsigned char*>(ws) + pl.counter_bytes;
+    pl.p.token = next_token();
 }
 
 Plan gemm_plan(const GemmInput& in, const GemmTuning& t) {

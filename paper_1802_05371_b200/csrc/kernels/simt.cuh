@@ -18,10 +18,10 @@
 //              each group stages w = max(u/k_l, k_s) columns per step so the
 //              block's staging footprint equals the resource model
 //              2*size*(m_l*u + u*n_l) of param_space.cpp:209-210
-//   k_g        grid slices (grid z); partials go to a workspace and the LAST
-//              block to finish a tile folds them in slice order (single
-//              launch, no memset, deterministic: the "merge pass" of
-//              backends.cpp:90-112 fused into the main kernel)
+//   k_g        grid slices (grid z); slices 0..nz-2 publish partial tiles
+//              to a workspace, the last slice's block folds them in slice
+//              order (single launch, no memset, deterministic: the "merge
+//              pass" of backends.cpp:90-112 fused into the main kernel)
 //
 // PARITY mode reproduces the reference summation order bit-for-bit
 // (separately rounded __fmul_rn/__fadd_rn, left folds from +0.0 in the order
@@ -48,8 +48,9 @@ struct SimtParams {
     std::int64_t kg_span;   // ceil(red / k_g)
     int nz;                 // non-empty grid slices (= gridDim.z)
     void* out;              // C / outputs
-    void* ws;               // k_g partials [nz][out_elems]
-    unsigned* counters;     // one per (row tile, col tile); zero between launches
+    void* ws;               // k_g partials [nz-1][out_elems]
+    unsigned long long* flags;  // [nz-1][tiles] publication tokens
+    unsigned long long token;   // unique per launch (never 0)
 };
 
 // ---- GEMM policy: A is M x K (K x M when ta), B is K x N (N x K when tb) ----
@@ -353,43 +354,62 @@ __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
             }
         return;
     }
+    // Slices 0..nz-2 publish their partial tile and a per-launch token; the
+    // block of the last slice (scheduled after every lower-z block has
+    // started, so the wait cannot deadlock) waits for all tokens and folds
+    // the partials in slice order, its own last (backends.cpp:320-325).
+    // Tokens are unique per launch, so the workspace never needs zeroing.
     T* ws = static_cast<T*>(p.ws);
-    if (owner)
+    const std::int64_t tiles = std::int64_t(gridDim.x) * gridDim.y;
+    const std::int64_t tile_id = std::int64_t(rt) * gridDim.x + ct;
+    if (g < p.nz - 1) {
+        if (owner)
 #pragma unroll
-        for (int i = 0; i < MS; ++i) {
-            const std::int64_t row = row0 + ty + i * p.tm;
-            if (row >= p.rows) continue;
+            for (int i = 0; i < MS; ++i) {
+                const std::int64_t row = row0 + ty + i * p.tm;
+                if (row >= p.rows) continue;
 #pragma unroll
-            for (int j = 0; j < NS; ++j) {
-                const std::int64_t oc = col_out[tx + j * p.tn];
-                if (oc >= 0) __stcg(ws + std::int64_t(g) * p.out_elems + prob.out_index(row, oc), blk[i * NS + j]);
+                for (int j = 0; j < NS; ++j) {
+                    const std::int64_t oc = col_out[tx + j * p.tn];
+                    if (oc >= 0) __stcg(ws + std::int64_t(g) * p.out_elems + prob.out_index(row, oc), blk[i * NS + j]);
+                }
+            }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long* flag = p.flags + std::int64_t(g) * tiles + tile_id;
+            asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(p.token) : "memory");
+        }
+        return;
+    }
+    if (tid == 0) {
+        for (int gg = 0; gg < p.nz - 1; ++gg) {
+            const unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + tile_id;
+            unsigned long long v;
+            while (true) {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(flag) : "memory");
+                if (v == p.token) break;
+                __nanosleep(64);
             }
         }
-    __threadfence();
-    __syncthreads();
-    __shared__ int s_last;
-    const std::int64_t tile_id = std::int64_t(rt) * gridDim.x + ct;
-    if (tid == 0) {
-        const unsigned prev = atomicAdd(p.counters + tile_id, 1u);
-        s_last = (prev == unsigned(p.nz - 1));
     }
     __syncthreads();
-    if (!s_last) return;
-    __threadfence();
     if (owner)
+#pragma unroll
         for (int i = 0; i < MS; ++i) {
             const std::int64_t row = row0 + ty + i * p.tm;
             if (row >= p.rows) continue;
+#pragma unroll
             for (int j = 0; j < NS; ++j) {
                 const std::int64_t oc = col_out[tx + j * p.tn];
                 if (oc < 0) continue;
                 const std::int64_t idx = prob.out_index(row, oc);
                 T v = T(0);
-                for (int gg = 0; gg < p.nz; ++gg) v = A::add(v, __ldcg(ws + std::int64_t(gg) * p.out_elems + idx));
-                out[idx] = v;
+                for (int gg = 0; gg < p.nz - 1; ++gg)
+                    v = A::add(v, __ldcg(ws + std::int64_t(gg) * p.out_elems + idx));
+                out[idx] = A::add(v, blk[i * NS + j]);
             }
         }
-    if (tid == 0) p.counters[tile_id] = 0u;  // leave the counter ready for the next launch
 }
 
 }  // namespace ktune_dev
