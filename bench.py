@@ -1,0 +1,397 @@
+"""Benchmark of the ISAAC GEMM/CONV hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): DeepBench fprop SGEMM M=2560 N=16 K=2560
+NN, fp32, with the input-aware tuned pick of the ISAAC tuple.  One step = one
+launch of the tuned kernel over resident operands, L2 flushed before each step
+(the 26 MB working set would otherwise live in the 126 MB L2); each step is
+bracketed by CUDA events on the launching stream and the step times are
+summed.  N>1 runs N independent replicas (the GEMM does not shard).
+
+--impl reference times the reference's own CPU executor (oracle/_ref: ktune
+execute_gemm<float> compiled from the untouched sources) on the same workload
+and tuple with every host core; it never touches the GPU.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = dict(name="deepbench-fprop-16", m=2560, n=16, k=2560, trans_a=False, trans_b=False, dtype="f32")
+PAPER_TUPLE = (2, 4, 64, 16, 16, 1, 1, 4)  # PAPER.md Table 5, DeepBench fprop N=16
+METRIC = "GEMM/CONV TFLOP/s of tuned pick vs cuBLAS & % B200 peak; tuning samples/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return {"hbm_gbs": p["hbm_gbs"], "bf16_tflops": p["bf16_tflops"], "source": "measured"}
+    except (OSError, KeyError, ValueError):
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._active = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _query(self):
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                 capture_output=True, text=True, timeout=5).stdout.strip()
+            f = [x.strip() for x in out.split(",")]
+            return dict(sm=float(f[1]), max=float(f[2]), hw=f[3], hw_thermal=f[4], sw_thermal=f[5], power_cap=f[6])
+        except Exception:
+            return None
+
+    def _run(self):
+        while not self._stop.is_set():
+            if self._active.is_set():
+                s = self._query()
+                if s is not None and self._active.is_set():
+                    self.samples.append(s)
+            self._stop.wait(0.1)
+
+    def start(self):
+        self._t.start()
+
+    def active(self, on: bool):
+        (self._active.set if on else self._active.clear)()
+
+    def stop(self):
+        self._stop.set()
+        self._t.join(timeout=10)
+        if not self.samples:  # region shorter than one query: take one now (device still warm)
+            s = self._query()
+            if s:
+                self.samples.append(s)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "n_samples": 0}
+        sms = sorted(s["sm"] for s in self.samples)
+        reasons = set()
+        for s in self.samples:
+            for key, name in (("hw", "hw_slowdown"), ("hw_thermal", "hw_thermal_slowdown"),
+                              ("sw_thermal", "sw_thermal_slowdown"), ("power_cap", "sw_power_cap")):
+                if s[key].lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": sms[len(sms) // 2], "sm_max_mhz": self.samples[0]["max"], "reasons": sorted(reasons),
+                "n_samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference CPU executor on the host cores
+# ---------------------------------------------------------------------------
+
+def reference_arm(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import ctypes
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_libs as O
+    w = WORKLOAD
+    flops = 2.0 * w["m"] * w["n"] * w["k"]
+    threads = os.cpu_count() or 1
+    budget_s = float(os.environ.get("KTUNE_REF_BUDGET_S", "60"))
+    lib = O.reference()
+    kind = "reference" if lib is not None else "port"
+    tv = (ctypes.c_int32 * 8)(*PAPER_TUPLE)
+    done_steps, total_s = 0, 0.0
+    if lib is not None:
+        g, s = ctypes.c_double(), ctypes.c_double()
+        # warm-up inside the call (one untimed execute per thread)
+        steps = max(1, args.steps)
+        t_begin = time.perf_counter()
+        while done_steps < steps and (time.perf_counter() - t_begin) < budget_s:
+            chunk = 1
+            rc = lib.ref_host_gemm_gflops(ctypes.c_int64(w["m"]), ctypes.c_int64(w["n"]), ctypes.c_int64(w["k"]), 0, 0,
+                                          tv, chunk, threads, ctypes.byref(g), ctypes.byref(s))
+            if rc != 0:
+                raise RuntimeError(lib.ref_last_error().decode())
+            done_steps += chunk
+            total_s += s.value
+        value = threads * done_steps * flops / total_s / 1e12
+        sample = (f"{done_steps} step(s) x {threads} concurrent execute_gemm<float> (reference ktune, "
+                  f"tuple {list(PAPER_TUPLE)}), each after an untimed warm-up; capped at {budget_s:.0f}s")
+    else:
+        import numpy as np
+        a, b = O.fill(0x5EED, w["m"] * w["k"], w["k"] * w["n"], "f32")
+        t0 = time.perf_counter()
+        while done_steps < max(1, args.steps) and time.perf_counter() - t0 < budget_s:
+            O.execute_gemm(w["m"], w["n"], w["k"], 0, 0, PAPER_TUPLE, a, b)
+            done_steps += 1
+        total_s = time.perf_counter() - t0
+        threads = 1
+        value = done_steps * flops / total_s / 1e12
+        sample = f"{done_steps} step(s) of the oracle port (single thread)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": done_steps,
+        "warmup": args.warmup, "ms_per_step": total_s / max(done_steps, 1) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded uniform [0,1))",
+        "config": {"workload": "SGEMM 2560x16x2560 NN fp32 (DeepBench fprop N=16), ISAAC tuple " + str(list(PAPER_TUPLE)),
+                   "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def cpu_baseline_sample(tuple_):
+    """The reference executor on the box's host cores, bounded to ~10-20 s."""
+    import ctypes
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_libs as O
+    w = WORKLOAD
+    flops = 2.0 * w["m"] * w["n"] * w["k"]
+    lib = O.reference()
+    threads = os.cpu_count() or 1
+    if lib is not None:
+        tv = (ctypes.c_int32 * 8)(*tuple_)
+        g, s = ctypes.c_double(), ctypes.c_double()
+        reps = int(os.environ.get("KTUNE_CPU_REPS", "8"))
+        rc = lib.ref_host_gemm_gflops(ctypes.c_int64(w["m"]), ctypes.c_int64(w["n"]), ctypes.c_int64(w["k"]), 0, 0, tv,
+                                      reps, threads, ctypes.byref(g), ctypes.byref(s))
+        if rc != 0:
+            raise RuntimeError(lib.ref_last_error().decode())
+        return {"value": threads * reps * flops / s.value / 1e12, "unit": "TFLOP/s", "cores": threads,
+                "kind": "reference",
+                "sample": f"{threads} threads x {reps} timed execute_gemm<float> (reference ktune from oracle/_ref, "
+                          f"tuple {list(tuple_)}) after one warm-up each; {s.value:.1f}s wall"}
+    a, b = O.fill(0x5EED, w["m"] * w["k"], w["k"] * w["n"], "f32")
+    t0 = time.perf_counter()
+    O.execute_gemm(w["m"], w["n"], w["k"], 0, 0, tuple_, a, b)
+    dt = time.perf_counter() - t0
+    return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": 1, "kind": "port",
+            "sample": "one execute of the oracle port (single thread)"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def our_arm(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1802_05371_b200 as K
+    from paper_1802_05371_b200.tuner import select_gemm
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w = WORKLOAD
+    inp = K.GemmInput(w["m"], w["n"], w["k"], w["dtype"], w["trans_a"], w["trans_b"])
+    hw = K.HardwareDescriptor.b200()
+    bounds = open(os.path.join(K.FIXTURES, "bounds", "gemm_b200.json")).read()
+
+    # input-aware pick (rank 0 tunes; every replica runs the same tuple)
+    t_sel = time.perf_counter()
+    if args.pick:
+        pick = [int(x) for x in args.pick.split(",")]
+        sel_info = {"screened": 0, "legal_space": None, "seconds": None, "fixed": True}
+    elif rank == 0:
+        sel = select_gemm(inp, hw, bounds, candidates=args.candidates, top_k=16, seed=0,
+                          extra=[K.GemmTuning(*PAPER_TUPLE)])
+        pick = sel.tuning.values()
+        sel_info = {"screened": sel.screened, "legal_space": sel.legal_space_size, "seconds": None}
+    else:
+        pick, sel_info = None, None
+    if ws > 1 and not args.pick:
+        obj = [pick, sel_info]
+        dist.broadcast_object_list(obj, src=0)
+        pick, sel_info = obj
+    sel_info["seconds"] = time.perf_counter() - t_sel
+    tuning = K.GemmTuning(*pick)
+
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    a = torch.rand(inp.m * inp.k, device=dev, generator=gen)
+    b = torch.rand(inp.k * inp.n, device=dev, generator=gen)
+    c = torch.empty(inp.m * inp.n, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    sp = stream.cuda_stream
+
+    def step():
+        K.execute_gemm(inp, tuning, a, b, c, mode="fast", stream=sp)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(3, args.warmup)):
+            K.l2_flush(sp)
+            step()
+    torch.cuda.synchronize(dev)
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks.active(True)
+    with torch.cuda.stream(stream):
+        for i in range(args.steps):
+            K.l2_flush(sp)
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+    torch.cuda.synchronize(dev)
+    clocks.active(False)
+    if ws > 1:
+        dist.barrier()
+    clocks.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(sum(step_ms))
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    flops = inp.flops
+    value = ws * args.steps * flops / (max_ms * 1e-3) / 1e12
+
+    # correctness of the timed pick (fast mode, vs the naive oracle on a row sample)
+    res = {}
+    if rank == 0:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import oracle_libs as O
+        rows = 64
+        an = a.view(inp.m, inp.k)[:rows].contiguous().cpu().numpy().ravel()
+        bn = b.cpu().numpy()
+        ref = O.naive_gemm(rows, inp.n, inp.k, 0, 0, an, bn)
+        res["max_rel_err_vs_naive_first64rows"] = O.max_rel_error(c.view(inp.m, inp.n)[:rows].cpu().numpy().ravel(), ref)
+
+    # e2e through the public host-buffer C-ABI (H2D A,B + kernel + D2H C each step)
+    e2e = None
+    if True:
+        ah = torch.rand(inp.m * inp.k, generator=torch.Generator().manual_seed(rank)).pin_memory()
+        bh = torch.rand(inp.k * inp.n, generator=torch.Generator().manual_seed(rank + 7)).pin_memory()
+        ch = torch.empty(inp.m * inp.n).pin_memory()
+        import ctypes
+        from paper_1802_05371_b200 import _lib
+        ic, tc = inp.c(), tuning.c()
+
+        def host_step():
+            _lib.call("ktune_execute_gemm", ctypes.byref(ic), ctypes.byref(tc), _lib.MODE_FAST, ah.data_ptr(),
+                      ah.numel(), bh.data_ptr(), bh.numel(), ch.data_ptr(), ch.numel())
+
+        for _ in range(max(3, args.warmup)):
+            host_step()
+        n_e2e = max(10, min(args.steps, 200))
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            host_step()
+        e2e_s = time.perf_counter() - t0
+        et = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": ws * n_e2e * flops / float(et.item()) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": (ah.numel() + bh.numel()) * 4, "d2h_bytes_per_step": ch.numel() * 4,
+               "steps": n_e2e, "timing": "host wall clock around the synchronous C-ABI call (ktune_execute_gemm)"}
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # context: cuBLAS SGEMM (TF32 off) on the same shape and flush protocol
+    torch.backends.cuda.matmul.allow_tf32 = False
+    A2, B2 = a.view(inp.m, inp.k), b.view(inp.k, inp.n)
+    cub_ms = []
+    with torch.cuda.stream(stream):
+        for i in range(max(3, args.warmup)):
+            torch.matmul(A2, B2)
+        for i in range(min(args.steps, 200)):
+            K.l2_flush(sp)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            torch.matmul(A2, B2)
+            s1.record(stream)
+            cub_ms.append((s0, s1))
+    torch.cuda.synchronize(dev)
+    cub = sum(s0.elapsed_time(s1) for s0, s1 in cub_ms) / len(cub_ms)
+    cublas_tflops = flops / (cub * 1e-3) / 1e12
+
+    pk = peaks()
+    avg_ms = total_ms / args.steps
+    alg_bytes = (inp.m * inp.k + inp.k * inp.n + inp.m * inp.n) * 4
+    achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(WORKLOAD["name"])
+        except ValueError:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": avg_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (torch.rand uniform [0,1) operands, resident in HBM)",
+        "config": {"workload": "SGEMM 2560x16x2560 NN fp32 (DeepBench fprop N=16, BASELINE configs[1])",
+                   "tuned_pick": pick, "selection": sel_info, "mode": "fast (FFMA SIMT family)",
+                   "l2": "flushed before every step (2x L2 write sweep, outside the event window)",
+                   "parallelism": f"replicas x{ws}"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+                     "algorithmic_bytes_per_launch": alg_bytes, "peak_source": pk["source"] + " burst copy"},
+        "context": {"cublas_sgemm_tflops": cublas_tflops, "ratio_vs_cublas": value / ws / cublas_tflops,
+                    "ffma_fp32_peak_tflops": 74.4},
+        "cpu_baseline": cpu_baseline_sample(PAPER_TUPLE if os.environ.get("KTUNE_CPU_TUPLE") != "pick" else pick),
+        "e2e": e2e,
+        "gpu_launches": 2 * args.steps,
+        "gpu_launches_detail": {"gemm": args.steps, "l2_flush": args.steps},
+        "clocks": clocks.summary(),
+        "correctness": res,
+    }
+    print(json.dumps(line))
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--candidates", type=int, default=3000)
+    ap.add_argument("--pick", default="", help="fixed tuple m_s,n_s,m_l,n_l,u,k_s,k_l,k_g (skips selection)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return our_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

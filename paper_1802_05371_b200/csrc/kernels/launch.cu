@@ -11,6 +11,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
+#include <functional>
+#include <initializer_list>
 #include <atomic>
 #include <chrono>
 #include <random>
@@ -58,14 +61,56 @@ struct Plan {
     dim3 grid;
     int col_tiles{0}, row_tiles{0};
     int ms{0}, ns{0}, ks{0};  // register tile used for the lookup (0 = generic)
+    bool arm{false}, brm{false};
     bool generic{false};
     std::size_t ws_bytes{0};
     std::size_t counter_bytes{0};
 };
 
-// rows/red/out: problem extents; ml,nl,ms,ns,ks,kl,kg,u: mapped tuple.
+int ilog2(std::int64_t v) {
+    int l = 0;
+    while ((std::int64_t(1) << (l + 1)) <= v) ++l;
+    return l;
+}
+
+// Largest vector width (elements, <= 16 bytes) dividing every requirement.
+int vec_width(int esize, std::initializer_list<std::int64_t> must_divide, std::initializer_list<const void*> ptrs,
+              int cap) {
+    int v = 16 / esize;
+    while (v > 1) {
+        bool ok = v <= cap;
+        for (std::int64_t x : must_divide) ok = ok && (x % v == 0);
+        for (const void* q : ptrs) ok = ok && (reinterpret_cast<std::uintptr_t>(q) % (std::uintptr_t(v) * esize) == 0);
+        if (ok) break;
+        v >>= 1;
+    }
+    return v;
+}
+
+// Reduction-slice alignment: every group start glo = g*kg_span + gx*kl_span
+// must be a multiple of the vector width for operands contiguous along the
+// reduction (checked for full slices and the ragged last one).
+std::int64_t slice_gcd_span(std::int64_t red, std::int64_t kg_span, int nz, int kl) {
+    const std::int64_t full_kl = ceil_div(kg_span, kl);
+    const std::int64_t last_len = red - std::int64_t(nz - 1) * kg_span;
+    const std::int64_t last_kl = ceil_div(last_len, kl);
+    std::int64_t g = kg_span;
+    for (std::int64_t x : {full_kl, last_kl}) {
+        std::int64_t a = g, b = x;
+        while (b) { std::int64_t t = a % b; a = b; b = t; }
+        g = a;
+    }
+    return g;
+}
+
+constexpr std::size_t kStageBudget = 48 * 1024;  // smem the pipeline aims to fill
+
+// rows/red/out: problem extents; ml,nl,ms,ns,ks,kl,kg,u: mapped tuple;
+// arm/brm: operand staging layouts; va/vb: vector widths (elements).
 Plan plan_simt(std::int64_t rows, std::int64_t red, std::int64_t out_elems, std::int64_t col_tiles, int ml, int nl,
-               int ms, int ns, int ks, int kl, int kg, int u, int esize, bool a_rc, bool b_rc) {
+               int ms, int ns, int ks, int kl, int kg, int u, int esize, bool arm, bool brm,
+               const std::function<int(int w, std::int64_t span_gcd)>& pick_va,
+               const std::function<int(int w, std::int64_t span_gcd)>& pick_vb) {
     Plan pl;
     auto& p = pl.p;
     p.rows = rows;
@@ -80,10 +125,25 @@ Plan plan_simt(std::int64_t rows, std::int64_t red, std::int64_t out_elems, std:
     p.tm = ml / ms;
     p.tn = nl / ns;
     p.w = std::max(u / kl, ks);
-    p.pad_a = a_rc ? 1 : 0;
-    p.pad_b = b_rc ? 1 : 0;
+    p.lw = ilog2(p.w);
+    p.lml = ilog2(ml);
+    p.lnl = ilog2(nl);
     p.kg_span = ceil_div(red, kg);
     p.nz = int(ceil_div(red, p.kg_span));
+    const std::int64_t span_gcd = slice_gcd_span(red, p.kg_span, p.nz, kl);
+    const int va = pick_va(p.w, span_gcd), vb = pick_vb(p.w, span_gcd);
+    p.lva = ilog2(va);
+    p.lvb = ilog2(vb);
+    const int pad = 16 / esize;  // keeps row-major rows 16-byte aligned
+    p.a_ld = arm ? p.w + pad : ml;
+    p.b_ld = brm ? p.w + pad : nl;
+    // group tiles rounded to 16 bytes so every cp.async / vector read stays aligned
+    p.a_group = int(ceil_div(arm ? ml * p.a_ld : p.w * p.a_ld, pad) * pad);
+    p.b_group = int(ceil_div(brm ? nl * p.b_ld : p.w * p.b_ld, pad) * pad);
+    p.a_stage = kl * p.a_group;
+    p.b_stage = kl * p.b_group;
+    pl.arm = arm;
+    pl.brm = brm;
     pl.threads = p.tm * p.tn * kl;
     if (pl.threads > 1024)
         throw unsupported_error("tuning needs " + std::to_string(pl.threads) + " threads per block; the device allows 1024");
@@ -92,15 +152,19 @@ Plan plan_simt(std::int64_t rows, std::int64_t red, std::int64_t out_elems, std:
     pl.row_tiles = int(ceil_div(rows, ml));
     if (pl.row_tiles > 65535 || p.nz > 65535) throw unsupported_error("grid too large for one launch");
     pl.grid = dim3(unsigned(pl.col_tiles), unsigned(pl.row_tiles), unsigned(p.nz));
-    const std::size_t stage =
-        std::size_t(2) * kl * p.w * std::size_t((ml + p.pad_a) + (nl + p.pad_b)) * std::size_t(esize);
+    const std::size_t stage_bytes = std::size_t(p.a_stage + p.b_stage) * std::size_t(esize);
+    const std::int64_t nsteps = ceil_div(ceil_div(p.kg_span, kl), p.w);
+    p.stages = int(std::clamp<std::size_t>(kStageBudget / stage_bytes, 2, 6));
+    p.stages = int(std::max<std::int64_t>(2, std::min<std::int64_t>(p.stages, nsteps + 1)));
     const std::size_t red_tile = std::size_t(ml) * nl * std::size_t(esize);
-    pl.smem = std::size_t(2) * nl * sizeof(std::int64_t) + std::max(stage, red_tile);
-    if (pl.smem > std::size_t(device_smem_optin()))
+    const std::size_t head = std::size_t(2) * nl * sizeof(std::int64_t);
+    const std::size_t optin = std::size_t(device_smem_optin());
+    while (p.stages > 2 && head + std::max(stage_bytes * p.stages, red_tile) > optin) --p.stages;
+    pl.smem = head + std::max(stage_bytes * std::size_t(p.stages), red_tile);
+    if (pl.smem > optin)
         throw unsupported_error("tuning needs " + std::to_string(pl.smem) + " bytes of shared memory; the device allows " +
-                                std::to_string(device_smem_optin()));
-    const bool in_envelope = ktune_dev::simt_thread_cap(ms, ns, ks) >= pl.threads;
-    pl.generic = !in_envelope;
+                                std::to_string(optin));
+    pl.generic = ktune_dev::simt_thread_cap(ms, ns, ks) < pl.threads;
     pl.ms = ms;
     pl.ns = ns;
     pl.ks = ks;
@@ -113,17 +177,30 @@ Plan plan_simt(std::int64_t rows, std::int64_t red, std::int64_t out_elems, std:
     return pl;
 }
 
+using Lookup = const void* (*)(int, int, int);
+
+Lookup gemm_lookup(Dtype dt, bool par, bool arm, bool brm) {
+    using namespace ktune_dev;
+    const int lay = (arm ? 0 : 1) + (brm ? 2 : 0);  // nn, tn, nt, tt
+    static const Lookup f32p[] = {&simt_gemm_f32_parity_nn, &simt_gemm_f32_parity_tn, &simt_gemm_f32_parity_nt,
+                                  &simt_gemm_f32_parity_tt};
+    static const Lookup f32f[] = {&simt_gemm_f32_fast_nn, &simt_gemm_f32_fast_tn, &simt_gemm_f32_fast_nt,
+                                  &simt_gemm_f32_fast_tt};
+    static const Lookup f64p[] = {&simt_gemm_f64_parity_nn, &simt_gemm_f64_parity_tn, &simt_gemm_f64_parity_nt,
+                                  &simt_gemm_f64_parity_tt};
+    static const Lookup f64f[] = {&simt_gemm_f64_fast_nn, &simt_gemm_f64_fast_tn, &simt_gemm_f64_fast_nt,
+                                  &simt_gemm_f64_fast_tt};
+    if (dt == Dtype::f32) return par ? f32p[lay] : f32f[lay];
+    return par ? f64p[lay] : f64f[lay];
+}
+
 const void* pick(bool conv, Dtype dt, Mode mode, Plan& pl) {
     using namespace ktune_dev;
     const bool par = (mode == Mode::parity);
-    const void* (*fn)(int, int, int) = nullptr;
-    if (!conv) {
-        if (dt == Dtype::f32) fn = par ? &simt_gemm_f32_parity : &simt_gemm_f32_fast;
-        else fn = par ? &simt_gemm_f64_parity : &simt_gemm_f64_fast;
-    } else {
-        if (dt == Dtype::f32) fn = par ? &simt_conv_f32_parity : &simt_conv_f32_fast;
-        else fn = par ? &simt_conv_f64_parity : &simt_conv_f64_fast;
-    }
+    Lookup fn;
+    if (!conv) fn = gemm_lookup(dt, par, pl.arm, pl.brm);
+    else if (dt == Dtype::f32) fn = par ? &simt_conv_f32_parity : &simt_conv_f32_fast;
+    else fn = par ? &simt_conv_f64_parity : &simt_conv_f64_fast;
     const void* k = pl.generic ? nullptr : fn(pl.ms, pl.ns, pl.ks);
     if (k == nullptr) {
         if (pl.ms * pl.ns * pl.ks > kGenericMaxAcc)
@@ -171,7 +248,9 @@ void bind_workspace(Plan& pl, void* ws, std::size_t ws_bytes) {
     pl.p.token = next_token();
 }
 
-Plan gemm_plan(const GemmInput& in, const GemmTuning& t) {
+// Pointers are only used for vector-width alignment (nullptr = assume the
+// 256-byte alignment of cudaMalloc, for workspace/launch-info queries).
+Plan gemm_plan(const GemmInput& in, const GemmTuning& t, const void* a = nullptr, const void* b = nullptr) {
     in.validate();
     t.validate();
     require_divisible(t.m_l, t.m_s, "m_l not divisible by m_s");
@@ -179,11 +258,19 @@ Plan gemm_plan(const GemmInput& in, const GemmTuning& t) {
     require_divisible(t.u, t.k_s, "u not divisible by k_s");
     if (in.dtype != Dtype::f32 && in.dtype != Dtype::f64)
         throw unsupported_error(std::string("simt family does not execute ") + to_string(in.dtype));
+    const int es = dtype_size_bytes(in.dtype);
+    const bool arm = !in.trans_a, brm = in.trans_b;
+    auto va = [&](int w, std::int64_t span_gcd) {
+        return arm ? vec_width(es, {in.k, span_gcd}, {a}, w) : vec_width(es, {in.m}, {a}, t.m_l);
+    };
+    auto vb = [&](int w, std::int64_t span_gcd) {
+        return brm ? vec_width(es, {in.k, span_gcd}, {b}, w) : vec_width(es, {in.n}, {b}, t.n_l);
+    };
     return plan_simt(in.m, in.k, in.m * in.n, ceil_div(in.n, t.n_l), t.m_l, t.n_l, t.m_s, t.n_s, t.k_s, t.k_l, t.k_g,
-                     t.u, dtype_size_bytes(in.dtype), !in.trans_a, in.trans_b);
+                     t.u, es, arm, brm, va, vb);
 }
 
-Plan conv_plan(const ConvInput& in, const ConvTuning& t) {
+Plan conv_plan(const ConvInput& in, const ConvTuning& t, const void* img = nullptr, const void* flt = nullptr) {
     in.validate();
     t.validate();
     require_divisible(t.k_l, t.k_s, "k_l not divisible by k_s");
@@ -193,10 +280,14 @@ Plan conv_plan(const ConvInput& in, const ConvTuning& t) {
     require_divisible(t.u, t.c_s, "u not divisible by c_s");
     if (in.dtype != Dtype::f32 && in.dtype != Dtype::f64)
         throw unsupported_error(std::string("simt family does not execute ") + to_string(in.dtype));
+    const int es = dtype_size_bytes(in.dtype);
     const std::int64_t col_tiles = ceil_div(in.p, t.p_l) * ceil_div(in.q, t.q_l) * ceil_div(in.n_batch, t.n_l);
+    auto va = [&](int, std::int64_t) { return vec_width(es, {in.k_filters}, {flt}, t.k_l); };
+    // gather chunks must be whole n-runs: n_l and N multiples of the width
+    auto vb = [&](int, std::int64_t) { return vec_width(es, {in.n_batch}, {img}, t.n_l); };
     return plan_simt(in.k_filters, in.c * in.r * in.s, in.k_filters * in.p * in.q * in.n_batch, col_tiles, t.k_l,
-                     t.p_l * t.q_l * t.n_l, t.k_s, t.p_s * t.q_s * t.n_s, t.c_s, t.c_l, t.c_g, t.u,
-                     dtype_size_bytes(in.dtype), false, false);
+                     t.p_l * t.q_l * t.n_l, t.k_s, t.p_s * t.q_s * t.n_s, t.c_s, t.c_l, t.c_g, t.u, es, false, false,
+                     va, vb);
 }
 
 template <typename T>
@@ -252,7 +343,7 @@ void gemm(const GemmInput& in, const GemmTuning& t, Mode mode, const void* a, co
         umma::gemm(in, t, a, b, c, ws, ws_bytes, stream);
         return;
     }
-    Plan pl = gemm_plan(in, t);
+    Plan pl = gemm_plan(in, t, a, b);
     bind_workspace(pl, ws, ws_bytes);
     if (in.dtype == Dtype::f32) launch_gemm_t<float>(in, pl, mode, a, b, c, stream);
     else launch_gemm_t<double>(in, pl, mode, a, b, c, stream);
@@ -260,7 +351,7 @@ void gemm(const GemmInput& in, const GemmTuning& t, Mode mode, const void* a, co
 
 void conv(const ConvInput& in, const ConvTuning& t, Mode mode, const void* images, const void* filters, void* outputs,
           void* ws, std::size_t ws_bytes, cudaStream_t stream) {
-    Plan pl = conv_plan(in, t);
+    Plan pl = conv_plan(in, t, images, filters);
     bind_workspace(pl, ws, ws_bytes);
     if (in.dtype == Dtype::f32) launch_conv_t<float>(in, t, pl, mode, images, filters, outputs, stream);
     else launch_conv_t<double>(in, t, pl, mode, images, filters, outputs, stream);

@@ -31,6 +31,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace ktune_dev {
@@ -44,7 +45,12 @@ struct SimtParams {
     int kl;                 // groups
     int tm, tn;             // threads per group along rows / cols
     int w;                  // staged reduction columns per group per step
-    int pad_a, pad_b;       // smem row pads
+    int lw, lml, lnl;       // log2 of w, ml, nl (all powers of two)
+    int lva, lvb;           // log2 of the cp.async vector width (elements) of A / B
+    int a_ld, b_ld;         // smem leading dimension of the A / B tiles
+    int a_group, b_group;   // elements of one group's A / B tile (incl. padding)
+    int a_stage, b_stage;   // elements of one pipeline stage (all groups)
+    int stages;             // cp.async pipeline depth (2..8)
     std::int64_t kg_span;   // ceil(red / k_g)
     int nz;                 // non-empty grid slices (= gridDim.z)
     void* out;              // C / outputs
@@ -61,9 +67,11 @@ struct GemmProblem {
     std::int64_t M, N, K;
     int ta, tb;
     int nl;
-    // A tile loads are contiguous along the reduction axis unless transposed.
-    __device__ bool a_red_contig() const { return !ta; }
-    __device__ bool b_red_contig() const { return tb; }
+    // Valid leading elements of a v-chunk of B columns starting at `base`
+    // (columns are contiguous global indices).
+    __device__ int b_cols_valid(std::int64_t base, int v) const {
+        return base < 0 ? 0 : int(min(std::int64_t(v), N - base));
+    }
     __device__ const T* a_addr(std::int64_t row, std::int64_t t) const {
         return ta ? a + t * M + row : a + row * K + t;
     }
@@ -91,8 +99,9 @@ struct ConvProblem {
     std::int64_t Nb, P, Q, K, C, R, S, H, W;
     int pl, ql, nlb;              // spatial block tile
     int tiles_q, tiles_n;         // column-tile grid decomposition
-    __device__ bool a_red_contig() const { return false; }
-    __device__ bool b_red_contig() const { return false; }
+    // The host only vectorises the gather when n-runs are whole chunks, so a
+    // chunk is entirely valid or entirely outside the tensor.
+    __device__ int b_cols_valid(std::int64_t base, int v) const { return base < 0 ? 0 : v; }
     __device__ const T* a_addr(std::int64_t row, std::int64_t t) const { return flt + t * K + row; }
     __device__ std::int64_t off(std::int64_t t) const {
         const std::int64_t rs = R * S;
@@ -154,16 +163,31 @@ struct Arith<double, false> {
 };
 
 // ---- cp.async (LDGSTS) with zero-fill for out-of-range elements ------------
-template <int BYTES>
-__device__ __forceinline__ void cp_async_zfill(void* smem, const void* gmem, bool valid) {
-    const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    const int src_bytes = valid ? BYTES : 0;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(saddr), "l"(gmem), "n"(BYTES),
-                 "r"(src_bytes));
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+// Copies the first src_bytes of a BYTES chunk and zero-fills the rest (an
+// invalid chunk has src_bytes 0 and reads nothing).
+template <int BYTES>
+__device__ __forceinline__ void cp_async_zfill(void* smem, const void* gmem, int src_bytes) {
+    const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem), "r"(src_bytes));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(saddr), "l"(gmem), "n"(BYTES),
+                     "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_wait_dyn(int n) {
+    switch (n) {
+        case 0: cp_async_wait<0>(); break;
+        case 1: cp_async_wait<1>(); break;
+        case 2: cp_async_wait<2>(); break;
+        case 3: cp_async_wait<3>(); break;
+        case 4: cp_async_wait<4>(); break;
+        case 5: cp_async_wait<5>(); break;
+        default: cp_async_wait<6>(); break;
+    }
+}
 
 // Generic (runtime-tile) kernels keep accumulators in local memory up to this
 // many per thread; larger register tiles are rejected at launch.
@@ -173,10 +197,15 @@ template <int MS, int NS, int KS>
 struct LaunchCap {
     // Keep the register budget honest: big register tiles only with few threads.
     static constexpr int acc = (MS == 0) ? kGenericMaxAcc : MS * NS * KS;
-    static constexpr int threads = (MS == 0) ? 1024 : (acc <= 16 ? 1024 : (acc <= 64 ? 512 : 256));
+    static constexpr int threads = (MS == 0) ? 1024 : (acc <= 16 ? 1024 : (acc <= 32 ? 512 : 256));
 };
 
-template <class Prob, typename T, int MS_, int NS_, int KS_, bool PARITY>
+// ARM: the A tile is staged row-major [row][kk] (global A contiguous along
+// the reduction, GEMM non-transposed A); otherwise k-major [kk][row].
+// BRM: the B tile is staged [col][kk] (GEMM transposed B); otherwise [kk][col].
+// Each operand is copied with cp.async chunks of 2^lv elements along its
+// global contiguous dimension, so smem keeps that dimension contiguous.
+template <class Prob, typename T, int MS_, int NS_, int KS_, bool PARITY, bool ARM, bool BRM>
 __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
     simt_kernel(const Prob prob, const SimtParams p) {
     constexpr bool RT = (MS_ == 0);  // runtime-tile generic kernel
@@ -188,13 +217,11 @@ __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
     using A = Arith<T, PARITY>;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    // smem: [col_base nl i64][col_out nl i64][As 2 x kl x w x (ml+pad_a)][Bs 2 x kl x w x (nl+pad_b)]
+    // smem: [col_base nl i64][col_out nl i64][stages x (A all groups, B all groups)]
     std::int64_t* col_base = reinterpret_cast<std::int64_t*>(smem_raw);
     std::int64_t* col_out = col_base + p.nl;
-    T* As = reinterpret_cast<T*>(col_out + p.nl);
-    const int a_ld = p.ml + p.pad_a, b_ld = p.nl + p.pad_b;
-    const int a_group = p.w * a_ld, b_group = p.w * b_ld;
-    T* Bs = As + 2 * p.kl * a_group;
+    T* stage_mem = reinterpret_cast<T*>(col_out + p.nl);
+    const int stage_elems = p.a_stage + p.b_stage;
 
     const int tid = threadIdx.x;
     const int nthreads = blockDim.x;
@@ -215,41 +242,67 @@ __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
     for (int x = tid; x < p.nl; x += nthreads) prob.column(ct, x, col_base[x], col_out[x]);
     __syncthreads();
 
-    // Stage step `st` for every group into buffer `buf`.
-    auto stage = [&](std::int64_t st, int buf) {
-        const int a_elems = p.kl * p.w * p.ml;
-        const bool a_rc = prob.a_red_contig();
-        for (int e = tid; e < a_elems; e += nthreads) {
-            const int gx = e / (p.w * p.ml);
-            const int rem = e - gx * (p.w * p.ml);
-            int kk, ii;
-            if (a_rc) { ii = rem / p.w; kk = rem - ii * p.w; }
-            else      { kk = rem / p.ml; ii = rem - kk * p.ml; }
+    // ---- stage loader --------------------------------------------------------
+    auto load_a = [&]<int BYTES>(std::int64_t st, T* dst) {
+        constexpr int V = BYTES / int(sizeof(T));
+        const int lchunks = p.lml + p.lw - p.lva;  // log2 chunks per group
+        const int total = p.kl << lchunks;
+        const int inner = ARM ? (p.lw - p.lva) : (p.lml - p.lva);
+        for (int e = tid; e < total; e += nthreads) {
+            const int gx = e >> lchunks;
+            const int c = e & ((1 << lchunks) - 1);
+            const int outer = c >> inner;
+            const int in = (c & ((1 << inner) - 1)) << p.lva;
+            const int ii = ARM ? outer : in;
+            const int kk = ARM ? in : outer;
             const std::int64_t glo = min(s_hi, s_lo + gx * kl_span);
             const std::int64_t ghi = min(s_hi, glo + kl_span);
             const std::int64_t t = glo + st * p.w + kk;
             const std::int64_t row = row0 + ii;
-            const bool ok = (t < ghi) && (row < p.rows);
-            const T* src = ok ? prob.a_addr(row, t) : reinterpret_cast<const T*>(p.out);
-            cp_async_zfill<sizeof(T)>(As + (buf * p.kl + gx) * a_group + kk * a_ld + ii, src, ok);
+            int n;
+            if constexpr (ARM) n = row < p.rows ? int(max(std::int64_t(0), min(std::int64_t(V), ghi - t))) : 0;
+            else n = t < ghi ? int(max(std::int64_t(0), min(std::int64_t(V), p.rows - row))) : 0;
+            const T* src = n > 0 ? prob.a_addr(row, t) : reinterpret_cast<const T*>(p.out);
+            T* d = dst + gx * p.a_group + (ARM ? ii * p.a_ld + kk : kk * p.a_ld + ii);
+            cp_async_zfill<BYTES>(d, src, n * int(sizeof(T)));
         }
-        const int b_elems = p.kl * p.w * p.nl;
-        const bool b_rc = prob.b_red_contig();
-        for (int e = tid; e < b_elems; e += nthreads) {
-            const int gx = e / (p.w * p.nl);
-            const int rem = e - gx * (p.w * p.nl);
-            int kk, xx;
-            if (b_rc) { xx = rem / p.w; kk = rem - xx * p.w; }
-            else      { kk = rem / p.nl; xx = rem - kk * p.nl; }
+    };
+    auto load_b = [&]<int BYTES>(std::int64_t st, T* dst) {
+        constexpr int V = BYTES / int(sizeof(T));
+        const int lchunks = p.lnl + p.lw - p.lvb;
+        const int total = p.kl << lchunks;
+        const int inner = BRM ? (p.lw - p.lvb) : (p.lnl - p.lvb);
+        for (int e = tid; e < total; e += nthreads) {
+            const int gx = e >> lchunks;
+            const int c = e & ((1 << lchunks) - 1);
+            const int outer = c >> inner;
+            const int in = (c & ((1 << inner) - 1)) << p.lvb;
+            const int xx = BRM ? outer : in;
+            const int kk = BRM ? in : outer;
             const std::int64_t glo = min(s_hi, s_lo + gx * kl_span);
             const std::int64_t ghi = min(s_hi, glo + kl_span);
             const std::int64_t t = glo + st * p.w + kk;
             const std::int64_t base = col_base[xx];
-            const bool ok = (t < ghi) && (base >= 0);
-            const T* src = ok ? prob.b_addr(t, base) : reinterpret_cast<const T*>(p.out);
-            cp_async_zfill<sizeof(T)>(Bs + (buf * p.kl + gx) * b_group + kk * b_ld + xx, src, ok);
+            int n;
+            if constexpr (BRM) n = base >= 0 ? int(max(std::int64_t(0), min(std::int64_t(V), ghi - t))) : 0;
+            else n = t < ghi ? prob.b_cols_valid(base, V) : 0;
+            const T* src = n > 0 ? prob.b_addr(t, base) : reinterpret_cast<const T*>(p.out);
+            T* d = dst + gx * p.b_group + (BRM ? xx * p.b_ld + kk : kk * p.b_ld + xx);
+            cp_async_zfill<BYTES>(d, src, n * int(sizeof(T)));
         }
-        cp_async_commit();
+    };
+    auto load_stage = [&](std::int64_t st, int slot) {
+        T* dst = stage_mem + slot * stage_elems;
+        switch (int(sizeof(T)) << p.lva) {
+            case 16: load_a.template operator()<16>(st, dst); break;
+            case 8: load_a.template operator()<8>(st, dst); break;
+            default: load_a.template operator()<int(sizeof(T))>(st, dst); break;
+        }
+        switch (int(sizeof(T)) << p.lvb) {
+            case 16: load_b.template operator()<16>(st, dst + p.a_stage); break;
+            case 8: load_b.template operator()<8>(st, dst + p.a_stage); break;
+            default: load_b.template operator()<int(sizeof(T))>(st, dst + p.a_stage); break;
+        }
     };
 
     T acc[ACC];
@@ -259,66 +312,178 @@ __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
     const std::int64_t my_lo = min(s_hi, s_lo + lg * kl_span);
     const std::int64_t my_hi = min(s_hi, my_lo + kl_span);
 
-    if (nsteps > 0) stage(0, 0);
+    // Ownership of rows / columns.  Operands staged contiguous along the
+    // reduction (ARM / BRM) are read 16 bytes (VK k-values) at a time per
+    // row, so threads own STRIDED rows (distinct rows of a warp fall in
+    // distinct bank groups; lanes sharing a row broadcast).  Operands staged
+    // contiguous along rows/cols are read as vectors across the thread's own
+    // BLOCKED rows/cols.  Ownership never changes what is summed, only who.
+    constexpr int VK = 16 / int(sizeof(T));
+    auto row_of = [&](int i) { return ARM ? ty + i * p.tm : ty * MS + i; };
+    auto col_of = [&](int j) { return BRM ? tx + j * p.tn : tx * NS + j; };
+
+    const int a_ld = p.a_ld, b_ld = p.b_ld;
+    const int a_rstep = p.tm * a_ld;  // ARM: distance between a thread's strided rows
+    const int b_cstep = p.tn * b_ld;  // BRM: distance between a thread's strided cols
+
+    // ---- multistage cp.async pipeline (one barrier per step) ----------------
+    const int S = p.stages;
+    for (int s = 0; s < S - 1; ++s) {
+        if (s < nsteps) load_stage(s, s);
+        cp_async_commit();
+    }
+    // vector path needs VK | w and k_s | VK (set = c % k_s inside a chunk)
+    const bool kvec = (KS_ > 0 && KS_ <= VK) && (p.w % VK) == 0;
+    int slot = 0;
     for (std::int64_t st = 0; st < nsteps; ++st) {
-        const int buf = int(st & 1);
-        if (st + 1 < nsteps) {
-            stage(st + 1, buf ^ 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
+        cp_async_wait_dyn(S - 2);
         __syncthreads();
+        {
+            const std::int64_t nxt = st + S - 1;
+            int nslot = slot + S - 1;
+            if (nslot >= S) nslot -= S;
+            if (nxt < nsteps) load_stage(nxt, nslot);
+            cp_async_commit();
+        }
         const std::int64_t k0 = my_lo + st * p.w;
         const int nv = int(max(std::int64_t(0), min(std::int64_t(p.w), my_hi - k0)));
-        const T* as = As + (buf * p.kl + lg) * a_group;
-        const T* bs = Bs + (buf * p.kl + lg) * b_group;
-        for (int kk0 = 0; kk0 < nv; kk0 += KS) {
+        const T* as = stage_mem + slot * stage_elems + lg * p.a_group;
+        const T* bs = stage_mem + slot * stage_elems + p.a_stage + lg * p.b_group;
+        if constexpr (!RT) {
+            if (kvec) {
+                // chunks of VK reduction columns; only the tail chunk is
+                // predicated (smem past nv holds zero-filled or stale values)
+                constexpr int VR = MS_ < VK ? MS_ : VK;  // row vector (k-major A)
+                constexpr int VC = NS_ < VK ? NS_ : VK;  // col vector (k-major B)
+                using VecK = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+                using Vec2 = typename std::conditional<sizeof(T) == 4, float2, double2>::type;
+                const T* a_base = as + (ARM ? ty * a_ld : ty * MS_);
+                const T* b_base = bs + (BRM ? tx * b_ld : tx * NS_);
+                auto chunk = [&]<bool FULL>(int kk0, int lim) {
+                    T ak[ARM ? MS_ * VK : 1];
+                    T bk[BRM ? NS_ * VK : 1];
+                    if constexpr (ARM) {
 #pragma unroll
-            for (int s = 0; s < (RT ? 1 : KS_); ++s) {
-                // generic kernel: iterate sets at runtime
-                for (int sr = 0; sr < (RT ? KS : 1); ++sr) {
-                    const int set = RT ? sr : s;
-                    const int kk = kk0 + set;
-                    if (kk < nv) {
-                        T av[RT ? 16 : (MS_ > 0 ? MS_ : 1)];
-                        T bv[RT ? 16 : (NS_ > 0 ? NS_ : 1)];
-                        if constexpr (RT) {
-                            // runtime tiles read operands on the fly
-                            for (int i = 0; i < MS; ++i) {
-                                const T a_ = as[kk * a_ld + ty + i * p.tm];
-                                for (int j = 0; j < NS; ++j) {
-                                    const T b_ = bs[kk * b_ld + tx + j * p.tn];
-                                    T& c_ = acc[(set * MS + i) * NS + j];
-                                    c_ = A::mac(c_, a_, b_);
+                        for (int i = 0; i < MS_; ++i) {
+                            const VecK v = *reinterpret_cast<const VecK*>(a_base + i * a_rstep + kk0);
+                            const T* vp = reinterpret_cast<const T*>(&v);
+#pragma unroll
+                            for (int c = 0; c < VK; ++c) ak[i * VK + c] = vp[c];
+                        }
+                    }
+                    if constexpr (BRM) {
+#pragma unroll
+                        for (int j = 0; j < NS_; ++j) {
+                            const VecK v = *reinterpret_cast<const VecK*>(b_base + j * b_cstep + kk0);
+                            const T* vp = reinterpret_cast<const T*>(&v);
+#pragma unroll
+                            for (int c = 0; c < VK; ++c) bk[j * VK + c] = vp[c];
+                        }
+                    }
+                    const T* ap = a_base + kk0 * a_ld;
+                    const T* bp = b_base + kk0 * b_ld;
+#pragma unroll
+                    for (int c = 0; c < VK; ++c) {
+                        if (FULL || c < lim) {
+                            T av[MS_], bv[NS_];
+                            if constexpr (ARM) {
+#pragma unroll
+                                for (int i = 0; i < MS_; ++i) av[i] = ak[i * VK + c];
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < MS_; i += VR) {
+                                    if constexpr (VR == 4) {
+                                        const float4 v = *reinterpret_cast<const float4*>(ap + i);
+                                        av[i] = v.x; av[i + 1] = v.y; av[i + 2] = v.z; av[i + 3] = v.w;
+                                    } else if constexpr (VR == 2) {
+                                        const Vec2 v = *reinterpret_cast<const Vec2*>(ap + i);
+                                        av[i] = v.x; av[i + 1] = v.y;
+                                    } else {
+                                        av[i] = ap[i];
+                                    }
                                 }
                             }
-                            (void)av;
-                            (void)bv;
-                        } else {
+                            if constexpr (BRM) {
 #pragma unroll
-                            for (int i = 0; i < MS_; ++i) av[i] = as[kk * a_ld + ty + i * p.tm];
+                                for (int j = 0; j < NS_; ++j) bv[j] = bk[j * VK + c];
+                            } else {
 #pragma unroll
-                            for (int j = 0; j < NS_; ++j) bv[j] = bs[kk * b_ld + tx + j * p.tn];
+                                for (int j = 0; j < NS_; j += VC) {
+                                    if constexpr (VC == 4) {
+                                        const float4 v = *reinterpret_cast<const float4*>(bp + j);
+                                        bv[j] = v.x; bv[j + 1] = v.y; bv[j + 2] = v.z; bv[j + 3] = v.w;
+                                    } else if constexpr (VC == 2) {
+                                        const Vec2 v = *reinterpret_cast<const Vec2*>(bp + j);
+                                        bv[j] = v.x; bv[j + 1] = v.y;
+                                    } else {
+                                        bv[j] = bp[j];
+                                    }
+                                }
+                            }
+                            constexpr int set_mask = KS_ - 1;  // KS_ divides VK: set = c % KS
 #pragma unroll
                             for (int i = 0; i < MS_; ++i)
 #pragma unroll
                                 for (int j = 0; j < NS_; ++j) {
-                                    T& c_ = acc[(set * MS_ + i) * NS_ + j];
+                                    T& c_ = acc[((c & set_mask) * MS_ + i) * NS_ + j];
+                                    c_ = A::mac(c_, av[i], bv[j]);
+                                }
+                        }
+                        if constexpr (!ARM) ap += a_ld;
+                        if constexpr (!BRM) bp += b_ld;
+                    }
+                };
+                const int nfull = nv & ~(VK - 1);
+                for (int kk0 = 0; kk0 < nfull; kk0 += VK) chunk.template operator()<true>(kk0, VK);
+                if (nfull < nv) chunk.template operator()<false>(nfull, nv - nfull);
+            } else {
+                // narrow stages (w < VK): scalar reads, k_s sets unrolled
+                for (int kk0 = 0; kk0 < nv; kk0 += KS_) {
+#pragma unroll
+                    for (int s = 0; s < KS_; ++s) {
+                        const int kk = kk0 + s;
+                        if (kk < nv) {
+                            T av[MS_], bv[NS_];
+#pragma unroll
+                            for (int i = 0; i < MS_; ++i)
+                                av[i] = ARM ? as[row_of(i) * a_ld + kk] : as[kk * a_ld + row_of(i)];
+#pragma unroll
+                            for (int j = 0; j < NS_; ++j)
+                                bv[j] = BRM ? bs[col_of(j) * b_ld + kk] : bs[kk * b_ld + col_of(j)];
+#pragma unroll
+                            for (int i = 0; i < MS_; ++i)
+#pragma unroll
+                                for (int j = 0; j < NS_; ++j) {
+                                    T& c_ = acc[(s * MS_ + i) * NS_ + j];
                                     c_ = A::mac(c_, av[i], bv[j]);
                                 }
                         }
                     }
                 }
             }
+        } else {
+            // generic runtime-tile kernel: scalar reads, sets iterated at runtime
+            for (int kk = 0; kk < nv; ++kk) {
+                const int set = kk % KS;  // (k - lo) % k_s since step starts are multiples of w, w % k_s == 0
+                for (int i = 0; i < MS; ++i) {
+                    const T a_ = ARM ? as[row_of(i) * a_ld + kk] : as[kk * a_ld + row_of(i)];
+                    for (int j = 0; j < NS; ++j) {
+                        const T b_ = BRM ? bs[col_of(j) * b_ld + kk] : bs[kk * b_ld + col_of(j)];
+                        T& c_ = acc[(set * MS + i) * NS + j];
+                        c_ = A::mac(c_, a_, b_);
+                    }
+                }
+            }
         }
-        __syncthreads();
+        if (++slot == S) slot = 0;
     }
+    cp_async_wait<0>();
+    __syncthreads();
 
     // ---- fold: k_s sets within a thread, then k_l groups in order ----------
     // (backends.cpp:311-318): blk = ((0 + g0s0) + g0s1) + ... + g1s0 + ...
     T blk[TILE];
-    T* red = As;  // reuse operand smem as an m_l x n_l tile
+    T* red = stage_mem;  // reuse the pipeline smem as an m_l x n_l tile
     const int red_ld = p.nl;
     const bool my_nonempty = my_lo < my_hi;
     for (int step = 0; step < p.kl; ++step) {
@@ -327,12 +492,12 @@ __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
             for (int i = 0; i < MS; ++i)
 #pragma unroll
                 for (int j = 0; j < NS; ++j) {
-                    T v = (step == 0) ? T(0) : red[(ty + i * p.tm) * red_ld + tx + j * p.tn];
+                    T v = (step == 0) ? T(0) : red[row_of(i) * red_ld + col_of(j)];
                     if (my_nonempty)
 #pragma unroll
                         for (int s = 0; s < KS; ++s) v = A::add(v, acc[(s * MS + i) * NS + j]);
                     blk[i * NS + j] = v;
-                    if (step + 1 < p.kl) red[(ty + i * p.tm) * red_ld + tx + j * p.tn] = v;
+                    if (step + 1 < p.kl) red[row_of(i) * red_ld + col_of(j)] = v;
                 }
         }
         __syncthreads();
@@ -345,10 +510,10 @@ __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
         if (owner)
 #pragma unroll
             for (int i = 0; i < MS; ++i) {
-                const std::int64_t row = row0 + ty + i * p.tm;
+                const std::int64_t row = row0 + row_of(i);
                 if (row >= p.rows) continue;
                 for (int j = 0; j < NS; ++j) {
-                    const std::int64_t oc = col_out[tx + j * p.tn];
+                    const std::int64_t oc = col_out[col_of(j)];
                     if (oc >= 0) out[prob.out_index(row, oc)] = A::add(T(0), blk[i * NS + j]);
                 }
             }
@@ -366,11 +531,11 @@ __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
         if (owner)
 #pragma unroll
             for (int i = 0; i < MS; ++i) {
-                const std::int64_t row = row0 + ty + i * p.tm;
+                const std::int64_t row = row0 + row_of(i);
                 if (row >= p.rows) continue;
 #pragma unroll
                 for (int j = 0; j < NS; ++j) {
-                    const std::int64_t oc = col_out[tx + j * p.tn];
+                    const std::int64_t oc = col_out[col_of(j)];
                     if (oc >= 0) __stcg(ws + std::int64_t(g) * p.out_elems + prob.out_index(row, oc), blk[i * NS + j]);
                 }
             }
@@ -397,11 +562,11 @@ __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
     if (owner)
 #pragma unroll
         for (int i = 0; i < MS; ++i) {
-            const std::int64_t row = row0 + ty + i * p.tm;
+            const std::int64_t row = row0 + row_of(i);
             if (row >= p.rows) continue;
 #pragma unroll
             for (int j = 0; j < NS; ++j) {
-                const std::int64_t oc = col_out[tx + j * p.tn];
+                const std::int64_t oc = col_out[col_of(j)];
                 if (oc < 0) continue;
                 const std::int64_t idx = prob.out_index(row, oc);
                 T v = T(0);

@@ -27,10 +27,15 @@ namespace ktune_dev {
 // simt_<kind>_<T>_<mode>.cu.  Returns nullptr for tiles outside the envelope;
 // (0,0,0) is the generic runtime-tile instantiation.
 #define KTUNE_DECLARE_LOOKUP(KIND, T, MODE) const void* simt_##KIND##_##T##_##MODE(int ms, int ns, int ks);
-KTUNE_DECLARE_LOOKUP(gemm, f32, parity)
-KTUNE_DECLARE_LOOKUP(gemm, f32, fast)
-KTUNE_DECLARE_LOOKUP(gemm, f64, parity)
-KTUNE_DECLARE_LOOKUP(gemm, f64, fast)
+#define KTUNE_DECLARE_GEMM_LOOKUPS(T, MODE)          \
+    KTUNE_DECLARE_LOOKUP(gemm, T, MODE##_nn)         \
+    KTUNE_DECLARE_LOOKUP(gemm, T, MODE##_tn)         \
+    KTUNE_DECLARE_LOOKUP(gemm, T, MODE##_nt)         \
+    KTUNE_DECLARE_LOOKUP(gemm, T, MODE##_tt)
+KTUNE_DECLARE_GEMM_LOOKUPS(f32, parity)
+KTUNE_DECLARE_GEMM_LOOKUPS(f32, fast)
+KTUNE_DECLARE_GEMM_LOOKUPS(f64, parity)
+KTUNE_DECLARE_GEMM_LOOKUPS(f64, fast)
 KTUNE_DECLARE_LOOKUP(conv, f32, parity)
 KTUNE_DECLARE_LOOKUP(conv, f32, fast)
 KTUNE_DECLARE_LOOKUP(conv, f64, parity)
@@ -40,7 +45,7 @@ KTUNE_DECLARE_LOOKUP(conv, f64, fast)
 inline int simt_thread_cap(int ms, int ns, int ks) {
     if (ms == 0) return 1024;
     const int acc = ms * ns * ks;
-    return acc <= 16 ? 1024 : (acc <= 64 ? 512 : 256);
+    return acc <= 16 ? 1024 : (acc <= 32 ? 512 : 256);
 }
 
 }  // namespace ktune_dev
