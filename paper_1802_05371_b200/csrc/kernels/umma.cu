@@ -1,17 +1,595 @@
-// umma.cu -- placeholder until the tcgen05 family lands.
+// umma.cu -- K4: the tensor-core GEMM family for sm_100a (bf16 / f16 / tf32
+// inputs, fp32 accumulation in TMEM, fp32 output).
+//
+// Replaces execute_gemm (backends.cpp:228-329) for the new dtypes.  Per CTA:
+//   warp 0      TMA producer: one elected lane streams A/B tiles into a ring
+//               of `stages` shared-memory slots (cp.async.bulk.tensor.2d,
+//               128/64/32-byte hardware swizzle, mbarrier complete_tx);
+//   warp 1      MMA issuer: allocates TMEM, one elected lane issues
+//               tcgen05.mma (kind::f16 or kind::tf32) per UMMA_K slice and
+//               frees each slot with tcgen05.commit;
+//   warps 2..5  epilogue: tcgen05.ld 32x32b rows of the fp32 accumulator,
+//               predicated vector stores (or split-K partial publication).
+//
+// ISAAC tuple -> tensor-core tile (the legality formulas of param_space.cpp
+// stay the space definition; tc_plan() adds the launchability rules):
+//   m_l   BLOCK_M = UMMA_M (128; 256 = CTA pair is the next variant)
+//   n_l   BLOCK_N = UMMA_N (16..256)
+//   u     BLOCK_K elements per pipeline stage (>= 32 bytes)
+//   k_g   split-K slices over the grid (deterministic ordered fix-up, as
+//         in the SIMT family)
+//   k_l, k_s, m_s, n_s  reserved for the CTA-pair / persistent variants;
+//         this build requires k_l = k_s = 1 and ignores m_s / n_s.
+// Operand majors follow the GEMM layout: A K-major unless trans_a, B
+// MN-major unless trans_b (both majors are native tcgen05 descriptor modes
+// for 16-bit and tf32 inputs).
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+#include <mutex>
+#include <string>
+
 #include "umma.hpp"
+
+namespace ktune_dev {
+namespace tc {
+
+struct TcParams {
+    int M, N, K;
+    int bm, bn, bk;
+    int stages;
+    int kb_total, kb_span, nz;
+    int a_kmajor, b_kmajor;
+    int a_sw, b_sw;               // swizzle span (bytes) of each operand's tiles
+    int a_boxes, b_boxes;         // TMA boxes per stage
+    unsigned a_box_bytes, b_box_bytes;
+    unsigned a_tile_bytes, b_tile_bytes;  // per stage, 1024-aligned
+    unsigned a_box_stride, b_box_stride;  // smem distance between boxes of one stage
+    unsigned idesc;
+    int umma_k_bytes;             // 32 (UMMA_K elements * element size)
+    int esize;
+    int tmem_cols;
+    float* C;
+    float* ws;
+    unsigned long long* flags;
+    unsigned long long token;
+    unsigned a_desc_hi, b_desc_hi;    // SBO | version | layout (descriptor bits 32..63)
+    unsigned a_desc_lbo, b_desc_lbo;  // LBO field in place (descriptor bits 16..29)
+    unsigned a_koff[8], b_koff[8];    // byte offset of UMMA_K slice kk inside a stage tile
+    long long* dbg;  // optional timeline probe (CTA 0): [kb][0]=producer issue, [kb][1]=mma start
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, unsigned long long* bar, int c0,
+                                            int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::
+            "r"(smem_u32(dst)),
+        "l"(reinterpret_cast<std::uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+template <int KIND>
+__device__ __forceinline__ void umma(unsigned tmem_d, std::uint64_t adesc, std::uint64_t bdesc, unsigned idesc,
+                                     unsigned accumulate) {
+    if constexpr (KIND == 0) {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+    } else {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+    }
+}
+
+__device__ __forceinline__ void umma_commit(unsigned long long* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(unsigned taddr, float* v) {
+    unsigned r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_ld16(unsigned taddr, float* v) {
+    unsigned r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ bool elect_one() {
+    unsigned pred = 0;
+    asm volatile(
+        "{\n.reg .b32 rx;\n.reg .pred px;\nelect.sync rx|px, 0xffffffff;\nselp.u32 %0, 1, 0, px;\n}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+
+constexpr int kThreads = 192;
+
+template <int KIND, int KSTEPS>
+__global__ void __launch_bounds__(kThreads, 1)
+    umma_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                     const TcParams p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-align the tile region (SW128 atoms repeat every 1024 bytes).
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
+                                                           ~std::uintptr_t(1023));
+    const unsigned stage_bytes = p.a_tile_bytes + p.b_tile_bytes;
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + std::size_t(p.stages) * stage_bytes);
+    unsigned long long* empty = full + p.stages;
+    unsigned long long* tmem_full = empty + p.stages;
+    unsigned* tmem_slot = reinterpret_cast<unsigned*>(tmem_full + 1);
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const int n0 = blockIdx.x * p.bn, m0 = blockIdx.y * p.bm, g = blockIdx.z;
+    const int kb_begin = g * p.kb_span;
+    const int kb_end = min(p.kb_total, kb_begin + p.kb_span);
+    const int nkb = kb_end - kb_begin;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < p.stages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        mbar_init(tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&tma_a)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&tma_b)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                     "r"(p.tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const unsigned tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer (whole warp loops, one lane issues) ----------------
+        int stage = 0;
+        unsigned phase = 0;
+        const int a_box_elems = p.a_sw / p.esize, b_box_elems = p.b_sw / p.esize;
+        const unsigned tx_bytes = p.a_boxes * p.a_box_bytes + p.b_boxes * p.b_box_bytes;
+        for (int kb = kb_begin; kb < kb_end; ++kb) {
+            mbar_wait(empty + stage, phase ^ 1u);
+            if (elect_one()) {
+                if (p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && kb - kb_begin < 64)
+                    p.dbg[2 * (kb - kb_begin)] = clock64();
+                unsigned char* sa = smem + std::size_t(stage) * stage_bytes;
+                unsigned char* sb = sa + p.a_tile_bytes;
+                mbar_expect_tx(full + stage, tx_bytes);
+                const int k0 = kb * p.bk;
+                for (int j = 0; j < p.a_boxes; ++j) {
+                    if (p.a_kmajor) tma_load_2d(sa + j * p.a_box_stride, &tma_a, full + stage, k0 + j * a_box_elems, m0);
+                    else tma_load_2d(sa + j * p.a_box_stride, &tma_a, full + stage, m0 + j * a_box_elems, k0);
+                }
+                for (int j = 0; j < p.b_boxes; ++j) {
+                    if (p.b_kmajor) tma_load_2d(sb + j * p.b_box_stride, &tma_b, full + stage, k0 + j * b_box_elems, n0);
+                    else tma_load_2d(sb + j * p.b_box_stride, &tma_b, full + stage, n0 + j * b_box_elems, k0);
+                }
+            }
+            __syncwarp();
+            if (++stage == p.stages) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (whole warp loops, one lane issues) ----------------
+        // Descriptors: constant high words and k-slice offsets come from the
+        // host; per k-block only the 14-bit start address changes.
+        int stage = 0;
+        unsigned phase = 0;
+        const unsigned base = smem_u32(smem);
+        for (int i = 0; i < nkb; ++i) {
+            mbar_wait(full + stage, phase);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            if (elect_one()) {
+                if (p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && i < 64) p.dbg[2 * i + 1] = clock64();
+                const unsigned sa = base + unsigned(stage) * stage_bytes;
+                const unsigned sb = sa + p.a_tile_bytes;
+#pragma unroll
+                for (int kk = 0; kk < KSTEPS; ++kk) {
+                    const std::uint64_t adesc =
+                        (std::uint64_t(p.a_desc_hi) << 32) | (((sa + p.a_koff[kk]) >> 4) & 0x3FFFu) | p.a_desc_lbo;
+                    const std::uint64_t bdesc =
+                        (std::uint64_t(p.b_desc_hi) << 32) | (((sb + p.b_koff[kk]) >> 4) & 0x3FFFu) | p.b_desc_lbo;
+                    umma<KIND>(tmem_base, adesc, bdesc, p.idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit(empty + stage);  // slot is free once these MMAs retire
+            }
+            __syncwarp();
+            if (++stage == p.stages) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+        if (elect_one()) umma_commit(tmem_full);
+        __syncwarp();
+    } else {
+        // ---------------- epilogue (warps 2..5) ----------------
+        const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+        const int row = m0 + quarter * 32 + lane;
+        const bool row_ok = row < p.M && quarter * 32 + lane < p.bm;
+        if (nkb > 0) {
+            mbar_wait(tmem_full, 0);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        }
+        const bool last = (g == p.nz - 1);
+        const std::int64_t tiles = std::int64_t(gridDim.x) * gridDim.y;
+        const std::int64_t tile_id = std::int64_t(blockIdx.y) * gridDim.x + blockIdx.x;
+        const std::int64_t MN = std::int64_t(p.M) * p.N;
+        if (last && p.nz > 1) {
+            if (threadIdx.x == 64) {
+                for (int gg = 0; gg < p.nz - 1; ++gg) {
+                    const unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + tile_id;
+                    unsigned long long v;
+                    while (true) {
+                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(flag) : "memory");
+                        if (v == p.token) break;
+                        __nanosleep(64);
+                    }
+                }
+            }
+            asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        }
+        const int chunk = p.bn >= 32 ? 32 : 16;
+        for (int c0 = 0; c0 < p.bn; c0 += chunk) {
+            float v[32];
+            const unsigned taddr = tmem_base + (unsigned(quarter * 32) << 16) + unsigned(c0);
+            if (nkb > 0) {
+                if (chunk == 32) tmem_ld32(taddr, v);
+                else tmem_ld16(taddr, v);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            }
+            if (!row_ok) continue;
+            const std::int64_t base = std::int64_t(row) * p.N + n0 + c0;
+            const int ncols = min(chunk, p.N - (n0 + c0));
+            if (ncols <= 0) continue;
+            if (p.nz == 1 || last) {
+                if (p.nz > 1) {
+                    for (int i = 0; i < ncols; ++i) {
+                        float acc = 0.f;
+                        for (int gg = 0; gg < p.nz - 1; ++gg) acc = __fadd_rn(acc, __ldcg(p.ws + gg * MN + base + i));
+                        v[i] = __fadd_rn(acc, v[i]);
+                    }
+                }
+                float* dst = p.C + base;
+                if (ncols == chunk && (reinterpret_cast<std::uintptr_t>(dst) & 15) == 0) {
+                    for (int i = 0; i < chunk; i += 4)
+                        *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                } else {
+                    for (int i = 0; i < ncols; ++i) dst[i] = v[i];
+                }
+            } else {
+                float* dst = p.ws + std::int64_t(g) * MN + base;
+                for (int i = 0; i < ncols; ++i) __stcg(dst + i, v[i]);
+            }
+        }
+        if (!last && p.nz > 1) {
+            __threadfence();
+            asm volatile("bar.sync 1, 128;\n" ::: "memory");
+            if (threadIdx.x == 64) {
+                unsigned long long* flag = p.flags + std::int64_t(g) * tiles + tile_id;
+                asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(p.token) : "memory");
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(p.tmem_cols));
+    }
+}
+
+}  // namespace tc
+}  // namespace ktune_dev
 
 namespace ktune {
 namespace umma {
 
-std::size_t gemm_workspace_bytes(const GemmInput&, const GemmTuning&) { return 0; }
+namespace {
 
-void gemm(const GemmInput& in, const GemmTuning&, const void*, const void*, void*, void*, std::size_t, cudaStream_t) {
-    throw unsupported_error(std::string("tensor-core family not built for ") + to_string(in.dtype));
+using ktune_dev::tc::TcParams;
+
+std::int64_t ceil_div(std::int64_t a, std::int64_t b) { return (a + b - 1) / b; }
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        dev::check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q),
+                   "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
+        if (p == nullptr || q != cudaDriverEntryPointSuccess) throw cuda_error("cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
 }
 
-dev::LaunchInfo gemm_launch_info(const GemmInput& in, const GemmTuning&) {
-    throw unsupported_error(std::string("tensor-core family not built for ") + to_string(in.dtype));
+int smem_optin() {
+    static int v = [] {
+        int dev = 0, x = 0;
+        dev::check(cudaGetDevice(&dev), "cudaGetDevice");
+        dev::check(cudaDeviceGetAttribute(&x, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "smem attr");
+        return x;
+    }();
+    return v;
+}
+
+struct TcPlan {
+    TcParams p{};
+    dim3 grid;
+    std::size_t smem{0};
+    std::size_t ws_bytes{0}, flag_bytes{0};
+    int kind{0};
+    int ksteps{4};
+};
+
+int pow2_ceil(int x) {
+    int v = 1;
+    while (v < x) v <<= 1;
+    return v;
+}
+
+TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
+    in.validate();
+    t.validate();
+    if (t.m_l % t.m_s != 0) throw std::invalid_argument("execute: m_l not divisible by m_s");
+    if (t.n_l % t.n_s != 0) throw std::invalid_argument("execute: n_l not divisible by n_s");
+    if (t.u % t.k_s != 0) throw std::invalid_argument("execute: u not divisible by k_s");
+    const int es = dtype_size_bytes(in.dtype);
+    TcPlan pl;
+    auto& p = pl.p;
+    pl.kind = in.dtype == Dtype::tf32 ? 1 : 0;
+    if (t.m_l != 128)
+        throw unsupported_error("tensor-core family: m_l must be 128 (UMMA_M) in this build, got " +
+                                std::to_string(t.m_l));
+    if (t.n_l < 16 || t.n_l > 256)
+        throw unsupported_error("tensor-core family: n_l must lie in [16, 256] (UMMA_N), got " + std::to_string(t.n_l));
+    if (t.k_l != 1 || t.k_s != 1)
+        throw unsupported_error("tensor-core family: k_l and k_s must be 1 in this build");
+    if (t.u * es < 32) throw unsupported_error("tensor-core family: u * element size must be >= 32 bytes");
+    if (in.m > 0x7fffffff || in.n > 0x7fffffff || in.k > 0x7fffffff)
+        throw unsupported_error("tensor-core family: dimensions must fit in 32 bits");
+    p.M = int(in.m);
+    p.N = int(in.n);
+    p.K = int(in.k);
+    p.bm = t.m_l;
+    p.bn = t.n_l;
+    p.bk = t.u;
+    p.esize = es;
+    p.umma_k_bytes = 32;
+    p.a_kmajor = in.trans_a ? 0 : 1;
+    p.b_kmajor = in.trans_b ? 1 : 0;
+    if (in.dtype == Dtype::tf32 && !(p.a_kmajor && p.b_kmajor))
+        throw unsupported_error("tensor-core family: tf32 needs K-major operands (trans_a = 0, trans_b = 1); "
+                                "MN-major tf32 tiles are not supported by this build");
+    // swizzle spans and TMA boxes
+    auto span_for = [](int bytes) { return bytes >= 128 ? 128 : (bytes >= 64 ? 64 : 32); };
+    if (p.a_kmajor) {
+        p.a_sw = span_for(p.bk * es);
+        p.a_boxes = p.bk * es / p.a_sw;
+        p.a_box_bytes = unsigned(p.a_sw) * p.bm;
+    } else {
+        p.a_sw = span_for(p.bm * es);
+        if (p.bm * es < p.a_sw) throw unsupported_error("tensor-core family: m_l too small for an MN-major A tile");
+        p.a_boxes = p.bm * es / p.a_sw;
+        p.a_box_bytes = unsigned(p.a_sw) * p.bk;
+    }
+    if (p.b_kmajor) {
+        p.b_sw = span_for(p.bk * es);
+        p.b_boxes = p.bk * es / p.b_sw;
+        p.b_box_bytes = unsigned(p.b_sw) * p.bn;
+    } else {
+        p.b_sw = span_for(p.bn * es);
+        if (p.bn * es < p.b_sw) throw unsupported_error("tensor-core family: n_l too small for an MN-major B tile");
+        p.b_boxes = p.bn * es / p.b_sw;
+        p.b_box_bytes = unsigned(p.b_sw) * p.bk;
+    }
+    p.a_box_stride = p.a_box_bytes;
+    p.b_box_stride = p.b_box_bytes;
+    p.a_tile_bytes = unsigned(ceil_div(std::int64_t(p.a_boxes) * p.a_box_bytes, 1024) * 1024);
+    p.b_tile_bytes = unsigned(ceil_div(std::int64_t(p.b_boxes) * p.b_box_bytes, 1024) * 1024);
+    // TMA: global strides must be multiples of 16 bytes
+    const std::int64_t a_ld = in.trans_a ? in.m : in.k, b_ld = in.trans_b ? in.k : in.n;
+    if ((a_ld * es) % 16 != 0 || (b_ld * es) % 16 != 0)
+        throw unsupported_error("tensor-core family: leading dimensions must be multiples of 16 bytes for TMA");
+    p.kb_total = int(ceil_div(in.k, p.bk));
+    p.kb_span = int(ceil_div(p.kb_total, t.k_g));
+    p.nz = int(ceil_div(p.kb_total, p.kb_span));
+    const std::size_t stage_bytes = std::size_t(p.a_tile_bytes) + p.b_tile_bytes;
+    const std::size_t extra = 1024 + 8 * 32 + 64;  // alignment slack + barriers + tmem slot
+    const std::size_t optin = std::size_t(smem_optin());
+    int stages = int((optin - extra) / stage_bytes);
+    stages = std::min(stages, 8);
+    stages = std::min<int>(stages, std::max(2, p.kb_span));
+    if (stages < 2) throw unsupported_error("tensor-core family: tile does not fit two pipeline stages in shared memory");
+    p.stages = stages;
+    pl.smem = extra + stage_bytes * std::size_t(stages);
+    p.tmem_cols = std::max(32, pow2_ceil(p.bn));
+    // instruction descriptor: F32 accumulate, operand formats, majors, N>>3, M>>4
+    const unsigned fmt = in.dtype == Dtype::bf16 ? 1u : (in.dtype == Dtype::f16 ? 0u : 2u);
+    p.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (unsigned(p.a_kmajor ? 0 : 1) << 15) |
+              (unsigned(p.b_kmajor ? 0 : 1) << 16) | (unsigned(p.bn >> 3) << 17) | (unsigned(p.bm >> 4) << 24);
+    // Shared-memory matrix descriptors (tcgen05 "version 1"): high word =
+    // SBO (8 rows x swizzle span) | version 1 | swizzle layout; LBO = 16 B for
+    // K-major (unused with swizzle), = box stride between MN atoms for
+    // MN-major.  Per UMMA_K slice (32 bytes of K) the start address moves
+    // 32 B inside a K-major swizzle atom (next box after sw bytes), or
+    // UMMA_K rows of sw bytes for MN-major.
+    auto hi_word = [](int sw) {
+        const unsigned layout = sw == 128 ? 2u : (sw == 64 ? 4u : 6u);
+        return ((unsigned(8 * sw) >> 4) & 0x3FFFu) | (1u << 14) | (layout << 29);
+    };
+    p.a_desc_hi = hi_word(p.a_sw);
+    p.b_desc_hi = hi_word(p.b_sw);
+    p.a_desc_lbo = ((p.a_kmajor ? 16u : p.a_box_stride) >> 4 & 0x3FFFu) << 16;
+    p.b_desc_lbo = ((p.b_kmajor ? 16u : p.b_box_stride) >> 4 & 0x3FFFu) << 16;
+    const int ksteps = p.bk * es / p.umma_k_bytes;
+    if (ksteps != 1 && ksteps != 2 && ksteps != 4 && ksteps != 8)
+        throw unsupported_error("tensor-core family: u * element size must be 32..256 bytes");
+    for (int kk = 0; kk < 8; ++kk) {
+        const unsigned kb = unsigned(kk * p.umma_k_bytes);
+        p.a_koff[kk] = p.a_kmajor ? (kb / p.a_sw) * p.a_box_stride + kb % p.a_sw : (kb / es) * p.a_sw;
+        p.b_koff[kk] = p.b_kmajor ? (kb / p.b_sw) * p.b_box_stride + kb % p.b_sw : (kb / es) * p.b_sw;
+    }
+    pl.ksteps = ksteps;
+    pl.grid = dim3(unsigned(ceil_div(in.n, p.bn)), unsigned(ceil_div(in.m, p.bm)), unsigned(p.nz));
+    if (pl.grid.y > 65535 || pl.grid.z > 65535) throw unsupported_error("grid too large for one launch");
+    if (p.nz > 1) {
+        pl.flag_bytes = (std::size_t(pl.grid.x) * pl.grid.y * std::size_t(p.nz - 1) * 8 + 255) / 256 * 256;
+        pl.ws_bytes = pl.flag_bytes + std::size_t(p.nz - 1) * std::size_t(in.m) * std::size_t(in.n) * 4;
+    }
+    return pl;
+}
+
+CUtensorMapDataType tma_dtype(Dtype d) {
+    switch (d) {
+        case Dtype::bf16: return CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        case Dtype::f16: return CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+        default: return CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    }
+}
+
+CUtensorMapSwizzle tma_swizzle(int sw) {
+    return sw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : (sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+}
+
+// 2-D map over a row-major [outer][inner] matrix; box = {box_inner, box_outer}.
+CUtensorMap make_map(const void* base, Dtype dt, std::int64_t inner, std::int64_t outer, int box_inner, int box_outer,
+                     int sw) {
+    CUtensorMap m;
+    const int es = dtype_size_bytes(dt);
+    cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
+    cuuint64_t strides[1] = {cuuint64_t(inner) * cuuint64_t(es)};
+    cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_outer)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&m, tma_dtype(dt), 2, const_cast<void*>(base), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, tma_swizzle(sw), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    return m;
+}
+
+unsigned long long next_token() {
+    static std::mutex mu;
+    static unsigned long long state = 0x243f6a8885a308d3ULL ^ reinterpret_cast<std::uintptr_t>(&mu);
+    std::lock_guard<std::mutex> lock(mu);
+    state += 0x9e3779b97f4a7c15ULL;
+    unsigned long long x = state;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    x ^= x >> 31;
+    return x ? x : 1;
+}
+
+}  // namespace
+
+std::size_t gemm_workspace_bytes(const GemmInput& in, const GemmTuning& t) { return tc_plan(in, t).ws_bytes; }
+
+dev::LaunchInfo gemm_launch_info(const GemmInput& in, const GemmTuning& t) {
+    TcPlan pl = tc_plan(in, t);
+    return dev::LaunchInfo{ktune_dev::tc::kThreads, pl.smem, int(pl.grid.x), int(pl.grid.y), int(pl.grid.z), false,
+                           "tcgen05"};
+}
+
+void gemm(const GemmInput& in, const GemmTuning& t, const void* a, const void* b, void* c, void* ws,
+          std::size_t ws_bytes, cudaStream_t stream) {
+    TcPlan pl = tc_plan(in, t);
+    auto& p = pl.p;
+    if ((reinterpret_cast<std::uintptr_t>(a) | reinterpret_cast<std::uintptr_t>(b)) % 16 != 0)
+        throw unsupported_error("tensor-core family: operand pointers must be 16-byte aligned for TMA");
+    p.C = static_cast<float*>(c);
+    if (const char* d = std::getenv("KTUNE_TC_DEBUG")) p.dbg = reinterpret_cast<long long*>(std::strtoull(d, nullptr, 0));
+    if (p.nz > 1) {
+        if (ws == nullptr || ws_bytes < pl.ws_bytes)
+            throw workspace_error("workspace of " + std::to_string(ws_bytes) + " bytes is smaller than the " +
+                                  std::to_string(pl.ws_bytes) + " bytes this tuning needs");
+        p.flags = static_cast<unsigned long long*>(ws);
+        p.ws = reinterpret_cast<float*>(static_cast<unsigned char*>(ws) + pl.flag_bytes);
+        p.token = next_token();
+    }
+    const int es = p.esize;
+    // A: K-major -> [M][K] rows, boxes {a_sw/es along K, bm}; MN-major -> [K][M], boxes {a_sw/es along M, bk}
+    CUtensorMap ma = p.a_kmajor ? make_map(a, in.dtype, in.k, in.m, p.a_sw / es, p.bm, p.a_sw)
+                                : make_map(a, in.dtype, in.m, in.k, p.a_sw / es, p.bk, p.a_sw);
+    CUtensorMap mb = p.b_kmajor ? make_map(b, in.dtype, in.k, in.n, p.b_sw / es, p.bn, p.b_sw)
+                                : make_map(b, in.dtype, in.n, in.k, p.b_sw / es, p.bk, p.b_sw);
+    using ktune_dev::tc::umma_gemm_kernel;
+    static const void* const kernels[2][4] = {
+        {reinterpret_cast<const void*>(&umma_gemm_kernel<0, 1>), reinterpret_cast<const void*>(&umma_gemm_kernel<0, 2>),
+         reinterpret_cast<const void*>(&umma_gemm_kernel<0, 4>), reinterpret_cast<const void*>(&umma_gemm_kernel<0, 8>)},
+        {reinterpret_cast<const void*>(&umma_gemm_kernel<1, 1>), reinterpret_cast<const void*>(&umma_gemm_kernel<1, 2>),
+         reinterpret_cast<const void*>(&umma_gemm_kernel<1, 4>), reinterpret_cast<const void*>(&umma_gemm_kernel<1, 8>)}};
+    const int ki = pl.ksteps == 1 ? 0 : (pl.ksteps == 2 ? 1 : (pl.ksteps == 4 ? 2 : 3));
+    const void* kern = kernels[pl.kind][ki];
+    {
+        static std::mutex mu;
+        static std::size_t configured[2][4] = {};
+        std::lock_guard<std::mutex> lock(mu);
+        if (configured[pl.kind][ki] < pl.smem) {
+            dev::check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)),
+                       "cudaFuncSetAttribute(umma smem)");
+            configured[pl.kind][ki] = pl.smem;
+        }
+    }
+    void* args[] = {&ma, &mb, &p};
+    dev::check(cudaLaunchKernel(kern, pl.grid, dim3(ktune_dev::tc::kThreads), args, pl.smem, stream), "umma launch");
 }
 
 }  // namespace umma
