@@ -186,6 +186,116 @@ KTUNE_API int ktune_measure_conv(const ktune_hw* hw, const ktune_conv_input* in,
 /* Evicts L2 with a write sweep larger than the cache (K8). */
 KTUNE_API int ktune_l2_flush(void* stream);
 
+
+/* ---- analytical cost model (backends.cpp:129-195; host oracle) ------------- */
+KTUNE_API int ktune_peak_gflops(const ktune_hw* hw, double* out);
+KTUNE_API int ktune_analytical_gflops_gemm(const ktune_hw* hw, const ktune_gemm_input* in, const ktune_gemm_tuning* t,
+                                           double* out);
+KTUNE_API int ktune_analytical_gflops_conv(const ktune_hw* hw, const ktune_conv_input* in, const ktune_conv_tuning* t,
+                                           double* out);
+
+/* ---- sampler (sampler.cpp:101-184); model JSON via ktune_last_text() ------- */
+KTUNE_API int ktune_calibrate_gemm(const ktune_hw* hw, const ktune_gemm_input* probe, const char* bounds_json,
+                                   int64_t n_uniform, uint64_t seed, double alpha);
+KTUNE_API int ktune_calibrate_conv(const ktune_hw* hw, const ktune_conv_input* probe, const char* bounds_json,
+                                   int64_t n_uniform, uint64_t seed, double alpha);
+KTUNE_API int ktune_acceptance_rate_gemm(const ktune_hw* hw, const ktune_gemm_input* probe, const char* sampler_json,
+                                         int64_t n_trials, uint64_t seed, double* rate);
+KTUNE_API int ktune_uniform_acceptance_rate_gemm(const ktune_hw* hw, const ktune_gemm_input* probe,
+                                                 const char* bounds_json, int64_t n_trials, uint64_t seed,
+                                                 double* rate);
+
+/* ---- input distributions (pipeline.hpp:86-118) ------------------------------ */
+typedef struct ktune_gemm_distribution {
+    const ktune_gemm_input* shapes; /* may be NULL when n_shapes == 0 */
+    int32_t n_shapes;
+    const double* weights; /* NULL = uniform over shapes */
+    double fixed_fraction;
+    int32_t use_ranges;
+    int32_t m_lo, m_hi, n_lo, n_hi, k_lo, k_hi;
+    int32_t dtype;
+    int32_t randomize_transpose;
+} ktune_gemm_distribution;
+
+typedef struct ktune_conv_distribution {
+    const ktune_conv_input* shapes;
+    int32_t n_shapes;
+    const double* weights;
+    double fixed_fraction;
+    int32_t use_ranges;
+    int32_t n_lo, n_hi, p_lo, p_hi, q_lo, q_hi, k_lo, k_hi, c_lo, c_hi;
+    const int32_t* rs_choices; /* n_rs (r, s) pairs */
+    int32_t n_rs;
+    int32_t dtype;
+} ktune_conv_distribution;
+
+/* ---- dataset generation (pipeline.cpp:463-556) ------------------------------ */
+/* The distinct (input, tuning) sequence generate_*_dataset measures, in order
+ * (the sampler RNG never depends on measurements, so it can be sharded). */
+KTUNE_API int ktune_predraw_gemm(const ktune_hw* hw, const char* bounds_json, const char* sampler_json,
+                                 const ktune_gemm_distribution* dist, int32_t n_samples, uint64_t seed,
+                                 ktune_gemm_input* inputs_out, ktune_gemm_tuning* tunings_out, int64_t* attempts,
+                                 int64_t* duplicates);
+KTUNE_API int ktune_predraw_conv(const ktune_hw* hw, const char* bounds_json, const char* sampler_json,
+                                 const ktune_conv_distribution* dist, int32_t n_samples, uint64_t seed,
+                                 ktune_conv_input* inputs_out, ktune_conv_tuning* tunings_out, int64_t* attempts,
+                                 int64_t* duplicates);
+/* Sequential generation with a backend (0 analytical, 1 b200, 2 b200-parity);
+ * CSV text (pipeline.hpp:53-57 header) via ktune_last_text(). */
+KTUNE_API int ktune_generate_gemm(const ktune_hw* hw, const char* bounds_json, const char* sampler_json,
+                                  const ktune_gemm_distribution* dist, int32_t n_samples, uint64_t seed,
+                                  int32_t backend, const ktune_measure_options* opts, int64_t* attempts,
+                                  int64_t* duplicates);
+/* Dataset CSV from measured records (rank 0 of a sharded run). */
+KTUNE_API int ktune_gemm_dataset_csv(const ktune_gemm_input* inputs, const ktune_gemm_tuning* tunings,
+                                     const double* gflops, int64_t n, const char* backend);
+KTUNE_API int ktune_conv_dataset_csv(const ktune_conv_input* inputs, const ktune_conv_tuning* tunings,
+                                     const double* gflops, int64_t n, const char* backend);
+/* Round-trips a dataset through the loader (validation + canonical text). */
+KTUNE_API int ktune_dataset_canonical(const char* csv_text, int32_t kind /* 0 gemm, 1 conv */);
+
+/* ---- MLP performance model (perf_model.cpp) ---------------------------------- */
+/* Trains on a dataset CSV on the GPU (K7); model JSON (ktune-mlp-1) via
+ * ktune_last_text().  history (2 doubles per epoch: train, val MSE) may be NULL. */
+KTUNE_API int ktune_mlp_train(const char* csv_text, int32_t kind, const int32_t* hidden, int32_t n_hidden,
+                              int32_t log_inputs, int32_t epochs, double learning_rate, int32_t batch_size,
+                              uint64_t seed, double validation_fraction, double* best_val_mse, int32_t* best_epoch,
+                              double* history);
+/* Glorot init (perf_model.cpp:57-79) as a model JSON. */
+KTUNE_API int ktune_mlp_init(int32_t input_dim, const int32_t* hidden, int32_t n_hidden, int32_t log_inputs,
+                             uint64_t seed, const char* feature_version);
+/* GPU forward of raw feature rows (MlpModel::predict_batch, bit-exact). */
+KTUNE_API int ktune_mlp_predict_rows(const char* model_json, const double* rows, int64_t n, int32_t dim, double* out);
+/* GPU candidate sweep for one GEMM / CONV input (MlpPredictor::predict_*). */
+KTUNE_API int ktune_mlp_predict_gemm(const char* model_json, const ktune_gemm_input* in,
+                                     const ktune_gemm_tuning* tunings, int64_t n, double* out);
+KTUNE_API int ktune_mlp_predict_conv(const char* model_json, const ktune_conv_input* in,
+                                     const ktune_conv_tuning* tunings, int64_t n, double* out);
+/* Host MSE of a model over a dataset CSV (mlp_evaluate). */
+KTUNE_API int ktune_mlp_evaluate(const char* model_json, const char* csv_text, int32_t kind, double* mse);
+
+/* ---- runtime selection (pipeline.cpp:649-723, :928-997) ---------------------- */
+/* infer_*: enumerate, predict (model_json NULL = analytical oracle predictor),
+ * re-measure top_k on `backend`, measured argmax; ktune-result-1 JSON via
+ * ktune_last_text(). */
+KTUNE_API int ktune_infer_gemm(const ktune_hw* hw, const char* bounds_json, const char* model_json,
+                               const ktune_gemm_input* in, int32_t top_k, int32_t backend,
+                               const ktune_measure_options* opts);
+KTUNE_API int ktune_infer_conv(const ktune_hw* hw, const char* bounds_json, const char* model_json,
+                               const ktune_conv_input* in, int32_t top_k, int32_t backend,
+                               const ktune_measure_options* opts);
+KTUNE_API int ktune_cache_key_gemm(const ktune_gemm_input* in);
+KTUNE_API int ktune_cache_key_conv(const ktune_conv_input* in);
+/* *found = 1 and the entry's JSON in ktune_last_text(), or *found = 0. */
+KTUNE_API int ktune_cache_lookup_gemm(const char* dir, const ktune_gemm_input* in, int* found);
+KTUNE_API int ktune_cache_lookup_conv(const char* dir, const ktune_conv_input* in, int* found);
+KTUNE_API int ktune_cache_store(const char* dir, const char* result_json);
+/* Runtime pick: in-memory map -> result cache (dir may be NULL) -> infer_gemm
+ * on the b200 backend, storing the result; writes the chosen tuning. */
+KTUNE_API int ktune_select_gemm(const ktune_hw* hw, const char* bounds_json, const char* model_json,
+                                const char* cache_dir, const ktune_gemm_input* in, int32_t top_k,
+                                ktune_gemm_tuning* chosen, int32_t* source /* 0 memory, 1 file, 2 inferred */);
+
 #ifdef __cplusplus
 }
 #endif

@@ -91,6 +91,21 @@ class MeasureOptionsC(ctypes.Structure):
                 ("flush_l2", ctypes.c_int32), ("seed", ctypes.c_uint64)]
 
 
+class GemmDistC(ctypes.Structure):
+    _fields_ = [("shapes", ctypes.c_void_p), ("n_shapes", ctypes.c_int32), ("weights", ctypes.c_void_p),
+                ("fixed_fraction", ctypes.c_double), ("use_ranges", ctypes.c_int32)] + [
+        (n, ctypes.c_int32) for n in ("m_lo", "m_hi", "n_lo", "n_hi", "k_lo", "k_hi", "dtype",
+                                       "randomize_transpose")]
+
+
+class ConvDistC(ctypes.Structure):
+    _fields_ = [("shapes", ctypes.c_void_p), ("n_shapes", ctypes.c_int32), ("weights", ctypes.c_void_p),
+                ("fixed_fraction", ctypes.c_double), ("use_ranges", ctypes.c_int32)] + [
+        (n, ctypes.c_int32) for n in ("n_lo", "n_hi", "p_lo", "p_hi", "q_lo", "q_hi", "k_lo", "k_hi", "c_lo",
+                                       "c_hi")] + [("rs_choices", ctypes.c_void_p), ("n_rs", ctypes.c_int32),
+                                                   ("dtype", ctypes.c_int32)]
+
+
 _P = ctypes.POINTER
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -127,6 +142,47 @@ _SIGNATURES = {
     "ktune_measure_conv": ([_P(HwC), _P(ConvInputC), _P(ConvTuningC), _P(MeasureOptionsC), _P(ctypes.c_double)],
                            ctypes.c_int),
     "ktune_l2_flush": ([_vp], ctypes.c_int),
+    "ktune_peak_gflops": ([_P(HwC), _P(ctypes.c_double)], ctypes.c_int),
+    "ktune_analytical_gflops_gemm": ([_P(HwC), _P(GemmInputC), _P(GemmTuningC), _P(ctypes.c_double)], ctypes.c_int),
+    "ktune_analytical_gflops_conv": ([_P(HwC), _P(ConvInputC), _P(ConvTuningC), _P(ctypes.c_double)], ctypes.c_int),
+    "ktune_calibrate_gemm": ([_P(HwC), _P(GemmInputC), ctypes.c_char_p, _i64, ctypes.c_uint64, ctypes.c_double],
+                             ctypes.c_int),
+    "ktune_calibrate_conv": ([_P(HwC), _P(ConvInputC), ctypes.c_char_p, _i64, ctypes.c_uint64, ctypes.c_double],
+                             ctypes.c_int),
+    "ktune_acceptance_rate_gemm": ([_P(HwC), _P(GemmInputC), ctypes.c_char_p, _i64, ctypes.c_uint64,
+                                    _P(ctypes.c_double)], ctypes.c_int),
+    "ktune_uniform_acceptance_rate_gemm": ([_P(HwC), _P(GemmInputC), ctypes.c_char_p, _i64, ctypes.c_uint64,
+                                            _P(ctypes.c_double)], ctypes.c_int),
+    "ktune_predraw_gemm": ([_P(HwC), ctypes.c_char_p, ctypes.c_char_p, _P(GemmDistC), ctypes.c_int32,
+                            ctypes.c_uint64, _vp, _vp, _P(_i64), _P(_i64)], ctypes.c_int),
+    "ktune_predraw_conv": ([_P(HwC), ctypes.c_char_p, ctypes.c_char_p, _P(ConvDistC), ctypes.c_int32,
+                            ctypes.c_uint64, _vp, _vp, _P(_i64), _P(_i64)], ctypes.c_int),
+    "ktune_generate_gemm": ([_P(HwC), ctypes.c_char_p, ctypes.c_char_p, _P(GemmDistC), ctypes.c_int32,
+                             ctypes.c_uint64, ctypes.c_int32, _P(MeasureOptionsC), _P(_i64), _P(_i64)],
+                            ctypes.c_int),
+    "ktune_gemm_dataset_csv": ([_vp, _vp, _vp, _i64, ctypes.c_char_p], ctypes.c_int),
+    "ktune_conv_dataset_csv": ([_vp, _vp, _vp, _i64, ctypes.c_char_p], ctypes.c_int),
+    "ktune_dataset_canonical": ([ctypes.c_char_p, ctypes.c_int32], ctypes.c_int),
+    "ktune_mlp_train": ([ctypes.c_char_p, ctypes.c_int32, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                         ctypes.c_double, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double, _P(ctypes.c_double),
+                         _P(ctypes.c_int32), _vp], ctypes.c_int),
+    "ktune_mlp_init": ([ctypes.c_int32, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_char_p],
+                       ctypes.c_int),
+    "ktune_mlp_predict_rows": ([ctypes.c_char_p, _vp, _i64, ctypes.c_int32, _vp], ctypes.c_int),
+    "ktune_mlp_predict_gemm": ([ctypes.c_char_p, _P(GemmInputC), _vp, _i64, _vp], ctypes.c_int),
+    "ktune_mlp_predict_conv": ([ctypes.c_char_p, _P(ConvInputC), _vp, _i64, _vp], ctypes.c_int),
+    "ktune_mlp_evaluate": ([ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int32, _P(ctypes.c_double)], ctypes.c_int),
+    "ktune_infer_gemm": ([_P(HwC), ctypes.c_char_p, ctypes.c_char_p, _P(GemmInputC), ctypes.c_int32,
+                          ctypes.c_int32, _P(MeasureOptionsC)], ctypes.c_int),
+    "ktune_infer_conv": ([_P(HwC), ctypes.c_char_p, ctypes.c_char_p, _P(ConvInputC), ctypes.c_int32,
+                          ctypes.c_int32, _P(MeasureOptionsC)], ctypes.c_int),
+    "ktune_cache_key_gemm": ([_P(GemmInputC)], ctypes.c_int),
+    "ktune_cache_key_conv": ([_P(ConvInputC)], ctypes.c_int),
+    "ktune_cache_lookup_gemm": ([ctypes.c_char_p, _P(GemmInputC), _P(ctypes.c_int)], ctypes.c_int),
+    "ktune_cache_lookup_conv": ([ctypes.c_char_p, _P(ConvInputC), _P(ctypes.c_int)], ctypes.c_int),
+    "ktune_cache_store": ([ctypes.c_char_p, ctypes.c_char_p], ctypes.c_int),
+    "ktune_select_gemm": ([_P(HwC), ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, _P(GemmInputC),
+                           ctypes.c_int32, _P(GemmTuningC), _P(ctypes.c_int32)], ctypes.c_int),
 }
 
 _lib = None
@@ -148,6 +204,11 @@ def lib():
             fn.restype = res
         _lib = handle
     return _lib
+
+
+def text() -> str:
+    """The library's thread-local text result (JSON / CSV / detail)."""
+    return lib().ktune_last_text().decode()
 
 
 def call(fn_name: str, *args) -> None:

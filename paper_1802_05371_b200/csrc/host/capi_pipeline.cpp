@@ -1,0 +1,454 @@
+// capi_pipeline.cpp -- extern "C" entry points of the tuning pipeline
+// (sampler, predraw/generation, datasets, MLP, runtime selection, cache);
+// declarations and reference citations in include/ktune_b200.h.
+
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+
+#include "capi_internal.hpp"
+#include "ktune/analytical.hpp"
+#include "ktune/mlp.hpp"
+#include "ktune/sampling.hpp"
+#include "ktune/tuner.hpp"
+
+using namespace ktune;
+using namespace ktune::capi;
+
+namespace {
+
+GemmBounds gemm_bounds(const char* json) {
+    return (json && json[0]) ? GemmBounds::from_json_text(json) : GemmBounds::defaults();
+}
+
+ConvBounds conv_bounds(const char* json) {
+    return (json && json[0]) ? ConvBounds::from_json_text(json) : ConvBounds::defaults();
+}
+
+GemmInputDistribution gemm_dist(const ktune_gemm_distribution* d) {
+    need(d, "distribution");
+    GemmInputDistribution g;
+    for (int i = 0; i < d->n_shapes; ++i) g.shapes.push_back(conv_in(d->shapes + i));
+    if (d->weights) g.weights.assign(d->weights, d->weights + d->n_shapes);
+    g.fixed_fraction = d->fixed_fraction;
+    g.use_ranges = d->use_ranges != 0;
+    g.m_lo = d->m_lo;
+    g.m_hi = d->m_hi;
+    g.n_lo = d->n_lo;
+    g.n_hi = d->n_hi;
+    g.k_lo = d->k_lo;
+    g.k_hi = d->k_hi;
+    g.dtype = dtype_of(d->dtype);
+    g.randomize_transpose = d->randomize_transpose != 0;
+    return g;
+}
+
+ConvInputDistribution conv_dist(const ktune_conv_distribution* d) {
+    need(d, "distribution");
+    ConvInputDistribution c;
+    for (int i = 0; i < d->n_shapes; ++i) c.shapes.push_back(conv_in(d->shapes + i));
+    if (d->weights) c.weights.assign(d->weights, d->weights + d->n_shapes);
+    c.fixed_fraction = d->fixed_fraction;
+    c.use_ranges = d->use_ranges != 0;
+    c.n_lo = d->n_lo;
+    c.n_hi = d->n_hi;
+    c.p_lo = d->p_lo;
+    c.p_hi = d->p_hi;
+    c.q_lo = d->q_lo;
+    c.q_hi = d->q_hi;
+    c.k_lo = d->k_lo;
+    c.k_hi = d->k_hi;
+    c.c_lo = d->c_lo;
+    c.c_hi = d->c_hi;
+    if (d->rs_choices) {
+        c.rs_choices.clear();
+        for (int i = 0; i < d->n_rs; ++i) c.rs_choices.push_back({d->rs_choices[2 * i], d->rs_choices[2 * i + 1]});
+    }
+    c.dtype = dtype_of(d->dtype);
+    return c;
+}
+
+ktune_gemm_input out_in(const GemmInput& in) {
+    return ktune_gemm_input{in.m, in.n, in.k, int32_t(in.dtype), in.trans_a ? 1 : 0, in.trans_b ? 1 : 0, 0};
+}
+
+ktune_conv_input out_in(const ConvInput& in) {
+    return ktune_conv_input{in.n_batch, in.p, in.q, in.k_filters, in.c, in.r, in.s, int32_t(in.dtype), 0};
+}
+
+ktune_gemm_tuning out_t(const GemmTuning& t) { return ktune_gemm_tuning{t.m_s, t.n_s, t.m_l, t.n_l, t.u, t.k_s, t.k_l, t.k_g}; }
+
+ktune_conv_tuning out_t(const ConvTuning& t) {
+    return ktune_conv_tuning{t.k_s, t.p_s, t.q_s, t.n_s, t.k_l, t.p_l, t.q_l, t.n_l, t.u, t.c_s, t.c_l, t.c_g};
+}
+
+std::unique_ptr<MeasurementBackend> make_backend(int32_t kind, const HardwareDescriptor& hw,
+                                                 const ktune_measure_options* opts) {
+    switch (kind) {
+        case 0: return std::make_unique<AnalyticalBackend>(hw);
+        case 1: {
+            MeasureOptions o = opts_of(opts);
+            if (!opts) o.mode = dev::Mode::fast;
+            return std::make_unique<B200Backend>(hw, o);
+        }
+        case 2: {
+            MeasureOptions o = opts_of(opts);
+            o.mode = dev::Mode::parity;
+            return std::make_unique<B200Backend>(hw, o);
+        }
+    }
+    throw std::invalid_argument("unknown backend " + std::to_string(kind) + " (0 analytical, 1 b200, 2 b200-parity)");
+}
+
+std::unique_ptr<PerfPredictor> make_predictor(const char* model_json, const HardwareDescriptor& hw) {
+    if (model_json && model_json[0]) return std::make_unique<MlpPredictor>(MlpModel::from_json_text(model_json));
+    return std::make_unique<AnalyticalPredictor>(hw);
+}
+
+// Runtime-selection memo: cache key -> chosen tuning (per process).
+std::mutex g_select_mu;
+std::map<std::string, GemmTuning> g_select_memo;
+
+}  // namespace
+
+extern "C" {
+
+int ktune_peak_gflops(const ktune_hw* hw, double* out) {
+    return guard([&] {
+        need(out, "out");
+        *out = peak_gflops(conv_hw(hw));
+    });
+}
+
+int ktune_analytical_gflops_gemm(const ktune_hw* hw, const ktune_gemm_input* in, const ktune_gemm_tuning* t,
+                                 double* out) {
+    return guard([&] {
+        need(out, "out");
+        *out = analytical_gflops(conv_in(in), conv_t(t), conv_hw(hw));
+    });
+}
+
+int ktune_analytical_gflops_conv(const ktune_hw* hw, const ktune_conv_input* in, const ktune_conv_tuning* t,
+                                 double* out) {
+    return guard([&] {
+        need(out, "out");
+        *out = analytical_gflops(conv_in(in), conv_t(t), conv_hw(hw));
+    });
+}
+
+int ktune_calibrate_gemm(const ktune_hw* hw, const ktune_gemm_input* probe, const char* bounds_json, int64_t n_uniform,
+                         uint64_t seed, double alpha) {
+    return guard([&] {
+        auto m = calibrate(make_legality(conv_in(probe), conv_hw(hw)), gemm_bounds(bounds_json).as_lists(), n_uniform,
+                           seed, alpha);
+        last_text() = m.to_json_text();
+    });
+}
+
+int ktune_calibrate_conv(const ktune_hw* hw, const ktune_conv_input* probe, const char* bounds_json, int64_t n_uniform,
+                         uint64_t seed, double alpha) {
+    return guard([&] {
+        auto m = calibrate(make_legality(conv_in(probe), conv_hw(hw)), conv_bounds(bounds_json).as_lists(), n_uniform,
+                           seed, alpha);
+        last_text() = m.to_json_text();
+    });
+}
+
+int ktune_acceptance_rate_gemm(const ktune_hw* hw, const ktune_gemm_input* probe, const char* sampler_json,
+                               int64_t n_trials, uint64_t seed, double* rate) {
+    return guard([&] {
+        need(sampler_json, "sampler_json");
+        need(rate, "rate");
+        *rate = acceptance_rate(CategoricalModel::from_json_text(sampler_json), make_legality(conv_in(probe), conv_hw(hw)),
+                                n_trials, seed);
+    });
+}
+
+int ktune_uniform_acceptance_rate_gemm(const ktune_hw* hw, const ktune_gemm_input* probe, const char* bounds_json,
+                                       int64_t n_trials, uint64_t seed, double* rate) {
+    return guard([&] {
+        need(rate, "rate");
+        *rate = uniform_acceptance_rate(gemm_bounds(bounds_json).as_lists(), make_legality(conv_in(probe), conv_hw(hw)),
+                                        n_trials, seed);
+    });
+}
+
+int ktune_predraw_gemm(const ktune_hw* hw, const char* bounds_json, const char* sampler_json,
+                       const ktune_gemm_distribution* dist, int32_t n_samples, uint64_t seed,
+                       ktune_gemm_input* inputs_out, ktune_gemm_tuning* tunings_out, int64_t* attempts,
+                       int64_t* duplicates) {
+    return guard([&] {
+        need(sampler_json, "sampler_json");
+        need(inputs_out, "inputs_out");
+        need(tunings_out, "tunings_out");
+        GenerateReport rep;
+        auto draws = predraw_gemm(CategoricalModel::from_json_text(sampler_json), gemm_dist(dist),
+                                  gemm_bounds(bounds_json), conv_hw(hw), n_samples, seed, &rep);
+        for (std::size_t i = 0; i < draws.size(); ++i) {
+            inputs_out[i] = out_in(draws[i].input);
+            tunings_out[i] = out_t(draws[i].tuning);
+        }
+        if (attempts) *attempts = rep.attempts;
+        if (duplicates) *duplicates = rep.duplicates_rejected;
+    });
+}
+
+int ktune_predraw_conv(const ktune_hw* hw, const char* bounds_json, const char* sampler_json,
+                       const ktune_conv_distribution* dist, int32_t n_samples, uint64_t seed,
+                       ktune_conv_input* inputs_out, ktune_conv_tuning* tunings_out, int64_t* attempts,
+                       int64_t* duplicates) {
+    return guard([&] {
+        need(sampler_json, "sampler_json");
+        need(inputs_out, "inputs_out");
+        need(tunings_out, "tunings_out");
+        GenerateReport rep;
+        auto draws = predraw_conv(CategoricalModel::from_json_text(sampler_json), conv_dist(dist),
+                                  conv_bounds(bounds_json), conv_hw(hw), n_samples, seed, &rep);
+        for (std::size_t i = 0; i < draws.size(); ++i) {
+            inputs_out[i] = out_in(draws[i].input);
+            tunings_out[i] = out_t(draws[i].tuning);
+        }
+        if (attempts) *attempts = rep.attempts;
+        if (duplicates) *duplicates = rep.duplicates_rejected;
+    });
+}
+
+int ktune_generate_gemm(const ktune_hw* hw, const char* bounds_json, const char* sampler_json,
+                        const ktune_gemm_distribution* dist, int32_t n_samples, uint64_t seed, int32_t backend,
+                        const ktune_measure_options* opts, int64_t* attempts, int64_t* duplicates) {
+    return guard([&] {
+        need(sampler_json, "sampler_json");
+        const HardwareDescriptor h = conv_hw(hw);
+        auto be = make_backend(backend, h, opts);
+        GenerateReport rep;
+        auto ds = generate_gemm_dataset(*be, CategoricalModel::from_json_text(sampler_json), gemm_dist(dist),
+                                        gemm_bounds(bounds_json), h, n_samples, seed, &rep);
+        if (attempts) *attempts = rep.attempts;
+        if (duplicates) *duplicates = rep.duplicates_rejected;
+        last_text() = to_csv_text(ds);
+    });
+}
+
+int ktune_gemm_dataset_csv(const ktune_gemm_input* inputs, const ktune_gemm_tuning* tunings, const double* gflops,
+                           int64_t n, const char* backend) {
+    return guard([&] {
+        need(backend, "backend");
+        GemmDataset ds;
+        for (int64_t i = 0; i < n; ++i)
+            ds.samples.push_back({conv_in(inputs + i), conv_t(tunings + i), gflops[i], backend, 0});
+        last_text() = to_csv_text(ds);
+    });
+}
+
+int ktune_conv_dataset_csv(const ktune_conv_input* inputs, const ktune_conv_tuning* tunings, const double* gflops,
+                           int64_t n, const char* backend) {
+    return guard([&] {
+        need(backend, "backend");
+        ConvDataset ds;
+        for (int64_t i = 0; i < n; ++i)
+            ds.samples.push_back({conv_in(inputs + i), conv_t(tunings + i), gflops[i], backend, 0});
+        last_text() = to_csv_text(ds);
+    });
+}
+
+int ktune_dataset_canonical(const char* csv_text, int32_t kind) {
+    return guard([&] {
+        need(csv_text, "csv_text");
+        last_text() = kind == 0 ? to_csv_text(gemm_dataset_from_csv_text(csv_text))
+                                : to_csv_text(conv_dataset_from_csv_text(csv_text));
+    });
+}
+
+int ktune_mlp_train(const char* csv_text, int32_t kind, const int32_t* hidden, int32_t n_hidden, int32_t log_inputs,
+                    int32_t epochs, double learning_rate, int32_t batch_size, uint64_t seed, double validation_fraction,
+                    double* best_val_mse, int32_t* best_epoch, double* history) {
+    return guard([&] {
+        need(csv_text, "csv_text");
+        const TrainingSet set = kind == 0 ? to_training_set(gemm_dataset_from_csv_text(csv_text))
+                                          : to_training_set(conv_dataset_from_csv_text(csv_text));
+        MlpArchitecture arch;
+        arch.input_dim = set.dim;
+        if (hidden && n_hidden > 0) arch.hidden_sizes.assign(hidden, hidden + n_hidden);
+        arch.log_inputs = log_inputs != 0;
+        TrainConfig cfg;
+        cfg.epochs = epochs;
+        cfg.learning_rate = learning_rate;
+        cfg.batch_size = batch_size;
+        cfg.rng_seed = seed;
+        cfg.validation_fraction = validation_fraction;
+        TrainResult r = mlp_train(set, arch, cfg);
+        if (best_val_mse) *best_val_mse = r.best_val_mse;
+        if (best_epoch) *best_epoch = r.best_epoch;
+        if (history)
+            for (std::size_t e = 0; e < r.history.size(); ++e) {
+                history[2 * e] = r.history[e].train_mse;
+                history[2 * e + 1] = r.history[e].val_mse;
+            }
+        MlpModel m;
+        m.feature_version = kind == 0 ? kGemmFeatureVersion : kConvFeatureVersion;
+        m.weights = r.weights;
+        last_text() = m.to_json_text();
+    });
+}
+
+int ktune_mlp_init(int32_t input_dim, const int32_t* hidden, int32_t n_hidden, int32_t log_inputs, uint64_t seed,
+                   const char* feature_version) {
+    return guard([&] {
+        MlpArchitecture arch;
+        arch.input_dim = input_dim;
+        if (hidden && n_hidden > 0) arch.hidden_sizes.assign(hidden, hidden + n_hidden);
+        arch.log_inputs = log_inputs != 0;
+        MlpModel m;
+        m.feature_version = feature_version ? feature_version : kGemmFeatureVersion;
+        m.weights = init_weights(arch, seed);
+        last_text() = m.to_json_text();
+    });
+}
+
+int ktune_mlp_predict_rows(const char* model_json, const double* rows, int64_t n, int32_t dim, double* out) {
+    return guard([&] {
+        need(model_json, "model_json");
+        const MlpModel m = MlpModel::from_json_text(model_json);
+        std::vector<std::vector<double>> r(static_cast<std::size_t>(n));
+        for (int64_t i = 0; i < n; ++i) r[std::size_t(i)].assign(rows + i * dim, rows + (i + 1) * dim);
+        std::vector<double> o;
+        m.predict_batch(r, o);
+        std::memcpy(out, o.data(), o.size() * sizeof(double));
+    });
+}
+
+int ktune_mlp_predict_gemm(const char* model_json, const ktune_gemm_input* in, const ktune_gemm_tuning* tunings,
+                           int64_t n, double* out) {
+    return guard([&] {
+        need(model_json, "model_json");
+        MlpPredictor p(MlpModel::from_json_text(model_json));
+        std::vector<GemmTuning> ts;
+        for (int64_t i = 0; i < n; ++i) ts.push_back(conv_t(tunings + i));
+        std::vector<double> o;
+        p.predict_gemm(conv_in(in), ts, o);
+        std::memcpy(out, o.data(), o.size() * sizeof(double));
+    });
+}
+
+int ktune_mlp_predict_conv(const char* model_json, const ktune_conv_input* in, const ktune_conv_tuning* tunings,
+                           int64_t n, double* out) {
+    return guard([&] {
+        need(model_json, "model_json");
+        MlpPredictor p(MlpModel::from_json_text(model_json));
+        std::vector<ConvTuning> ts;
+        for (int64_t i = 0; i < n; ++i) ts.push_back(conv_t(tunings + i));
+        std::vector<double> o;
+        p.predict_conv(conv_in(in), ts, o);
+        std::memcpy(out, o.data(), o.size() * sizeof(double));
+    });
+}
+
+int ktune_mlp_evaluate(const char* model_json, const char* csv_text, int32_t kind, double* mse) {
+    return guard([&] {
+        need(model_json, "model_json");
+        need(csv_text, "csv_text");
+        need(mse, "mse");
+        const MlpModel m = MlpModel::from_json_text(model_json);
+        const TrainingSet set = kind == 0 ? to_training_set(gemm_dataset_from_csv_text(csv_text))
+                                          : to_training_set(conv_dataset_from_csv_text(csv_text));
+        *mse = mlp_evaluate(m.weights, set);
+    });
+}
+
+int ktune_infer_gemm(const ktune_hw* hw, const char* bounds_json, const char* model_json, const ktune_gemm_input* in,
+                     int32_t top_k, int32_t backend, const ktune_measure_options* opts) {
+    return guard([&] {
+        const HardwareDescriptor h = conv_hw(hw);
+        auto be = make_backend(backend, h, opts);
+        auto pred = make_predictor(model_json, h);
+        last_text() = to_json_text(infer_gemm(*pred, conv_in(in), h, gemm_bounds(bounds_json), top_k, *be));
+    });
+}
+
+int ktune_infer_conv(const ktune_hw* hw, const char* bounds_json, const char* model_json, const ktune_conv_input* in,
+                     int32_t top_k, int32_t backend, const ktune_measure_options* opts) {
+    return guard([&] {
+        const HardwareDescriptor h = conv_hw(hw);
+        auto be = make_backend(backend, h, opts);
+        auto pred = make_predictor(model_json, h);
+        last_text() = to_json_text(infer_conv(*pred, conv_in(in), h, conv_bounds(bounds_json), top_k, *be));
+    });
+}
+
+int ktune_cache_key_gemm(const ktune_gemm_input* in) {
+    return guard([&] { last_text() = cache_key(conv_in(in)); });
+}
+
+int ktune_cache_key_conv(const ktune_conv_input* in) {
+    return guard([&] { last_text() = cache_key(conv_in(in)); });
+}
+
+int ktune_cache_lookup_gemm(const char* dir, const ktune_gemm_input* in, int* found) {
+    return guard([&] {
+        need(dir, "dir");
+        need(found, "found");
+        auto r = ResultCache(dir).lookup(conv_in(in));
+        *found = r ? 1 : 0;
+        last_text() = r ? to_json_text(*r) : std::string();
+    });
+}
+
+int ktune_cache_lookup_conv(const char* dir, const ktune_conv_input* in, int* found) {
+    return guard([&] {
+        need(dir, "dir");
+        need(found, "found");
+        auto r = ResultCache(dir).lookup(conv_in(in));
+        *found = r ? 1 : 0;
+        last_text() = r ? to_json_text(*r) : std::string();
+    });
+}
+
+int ktune_cache_store(const char* dir, const char* result_json) {
+    return guard([&] {
+        need(dir, "dir");
+        need(result_json, "result_json");
+        const std::string text(result_json);
+        if (text.find("\"kind\": \"conv\"") != std::string::npos)
+            ResultCache(dir).store(conv_result_from_json_text(text));
+        else
+            ResultCache(dir).store(gemm_result_from_json_text(text));
+    });
+}
+
+int ktune_select_gemm(const ktune_hw* hw, const char* bounds_json, const char* model_json, const char* cache_dir,
+                      const ktune_gemm_input* in, int32_t top_k, ktune_gemm_tuning* chosen, int32_t* source) {
+    return guard([&] {
+        need(chosen, "chosen");
+        const GemmInput input = conv_in(in);
+        const std::string key = cache_key(input);
+        {
+            std::lock_guard<std::mutex> lock(g_select_mu);
+            auto it = g_select_memo.find(key);
+            if (it != g_select_memo.end()) {
+                *chosen = out_t(it->second);
+                if (source) *source = 0;
+                return;
+            }
+        }
+        std::optional<GemmInferenceResult> r;
+        int32_t src = 1;
+        if (cache_dir && cache_dir[0]) r = ResultCache(cache_dir).lookup(input);
+        if (!r) {
+            const HardwareDescriptor h = conv_hw(hw);
+            B200Backend be(h);
+            auto pred = make_predictor(model_json, h);
+            r = infer_gemm(*pred, input, h, gemm_bounds(bounds_json), top_k, be);
+            if (cache_dir && cache_dir[0]) ResultCache(cache_dir).store(*r);
+            src = 2;
+        }
+        {
+            std::lock_guard<std::mutex> lock(g_select_mu);
+            g_select_memo[key] = r->chosen;
+        }
+        *chosen = out_t(r->chosen);
+        if (source) *source = src;
+    });
+}
+
+}  // extern "C"
