@@ -197,6 +197,170 @@ def cpu_baseline_sample(tuple_):
 # our arm
 # ---------------------------------------------------------------------------
 
+def timed_ms(launch, reps, stream, flush=True):
+    """Mean device time of `launch` (CUDA events on `stream`, L2 flushed
+    before each repetition, outside the event window)."""
+    import torch
+
+    import paper_1802_05371_b200 as K
+    evs = []
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            launch()
+        for _ in range(reps):
+            if flush:
+                K.l2_flush(stream.cuda_stream)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            launch()
+            s1.record(stream)
+            evs.append((s0, s1))
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in evs) / len(evs)
+
+
+def tuning_loop(args, ws, rank, dev):
+    """BASELINE configs[4] (bounded): the README tuning pipeline on the B200
+    descriptor -- calibrated sampler, tuning samples pre-drawn and LPT-sharded
+    over the ranks, measured on each GPU, one NCCL all-gather of {index,
+    gflops} records; then (rank 0) the GPU MLP fit and the runtime pick."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1802_05371_b200 as K
+    from paper_1802_05371_b200 import pipeline as P
+    hw = K.HardwareDescriptor.b200()
+    bounds = open(os.path.join(K.FIXTURES, "bounds", "gemm_b200.json")).read()
+    sampler = P.calibrate(K.GemmInput(512, 512, 512), hw, bounds, 100000, 11)
+    dist_ = P.GemmInputDistribution(shapes=P.gemm_shapes_from_table(os.path.join(K.FIXTURES, "shapes",
+                                                                                 "benchmarks.json")),
+                                    fixed_fraction=0.25)
+    n = args.tuning_samples * ws
+    K.measure(K.GemmInput(256, 256, 256), K.GemmTuning(2, 2, 32, 32, 8, 1, 1, 1), hw)  # load modules, buffers
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    csv, stats = P.generate_sharded(sampler, dist_, hw, bounds, n, 42, backend="b200", device=dev)
+    torch.cuda.synchronize(dev)
+    el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    secs = float(el.item())
+    out = {"samples": n, "samples_per_s": n / secs, "seconds": secs, "per_gpu_samples": args.tuning_samples,
+           "scaling": "weak", "predraw_s": stats["predraw_s"],
+           "gather": "NCCL all_gather_into_tensor of {index, gflops} records" if ws > 1 else "single rank",
+           "pipeline": "README walkthrough on fixtures/hw/b200.json + bounds/gemm_b200.json, seed 42, "
+                       "fixture shapes at 0.25, f32 (reference: generate_gemm_dataset, pipeline.cpp:463-509)",
+           "timing": "host wall clock of the sharded measurement loop, max over ranks",
+           "reference_cpu_samples_per_s_per_core": 0.0068}
+    if rank == 0:
+        t1 = time.perf_counter()
+        fit = P.train_mlp(csv, epochs=60, seed=7)
+        out["mlp_fit"] = {"rows": n, "epochs": 60, "seconds": time.perf_counter() - t1,
+                          "best_val_mse": fit.best_val_mse, "where": "GPU (K7, one CTA)"}
+        inp = K.GemmInput(2560, 32, 2560, "f32")
+        space = K.enumerate_legal(inp, hw, bounds)
+        P.mlp_predict(fit.model_json, inp, space[:1000])
+        t2 = time.perf_counter()
+        P.mlp_predict(fit.model_json, inp, space)
+        sweep = time.perf_counter() - t2
+        t3 = time.perf_counter()
+        pick, src = P.select_gemm(inp, hw, bounds, fit.model_json, None, top_k=20)
+        cold = time.perf_counter() - t3
+        t4 = time.perf_counter()
+        pick2, src2 = P.select_gemm(inp, hw, bounds, fit.model_json, None, top_k=20)
+        warm = time.perf_counter() - t4
+        out["runtime_pick"] = {"input": "2560x32x2560 f32 NN", "legal_space": len(space),
+                               "sweep_predictions_per_s": len(space) / sweep,
+                               "cold_pick_ms": cold * 1e3, "cold_source": src, "warm_pick_us": warm * 1e6,
+                               "warm_source": src2, "top_k": 20, "chosen": pick.values()}
+    return out
+
+
+def other_configs(stream, dev):
+    """The other BASELINE configs on this GPU (rank 0): tensor-core skinny
+    and square GEMMs, the ResNet-style convolution, C1's fixed tuple."""
+    import torch
+
+    import paper_1802_05371_b200 as K
+    from paper_1802_05371_b200.tuner import select_conv, select_gemm
+    pk = peaks()
+    hw = K.HardwareDescriptor.b200()
+    sp = stream.cuda_stream
+    res = {}
+    g = torch.Generator(device=dev).manual_seed(11)
+
+    def rnd(n, dt):
+        return torch.rand(n, device=dev, generator=g).to(dt)
+
+    # C2 bf16: skinny DeepBench on the tensor-core family (tuned over gemm_b200_tc.json)
+    inp = K.GemmInput(2560, 16, 2560, "bf16")
+    a, b = rnd(inp.m * inp.k, torch.bfloat16), rnd(inp.k * inp.n, torch.bfloat16)
+    c = torch.empty(inp.m * inp.n, device=dev)
+    tc_bounds = open(os.path.join(K.FIXTURES, "bounds", "gemm_b200_tc.json")).read()
+    sel = select_gemm(inp, hw, tc_bounds, candidates=200, top_k=8)
+    ms = timed_ms(lambda: K.execute_gemm(inp, sel.tuning, a, b, c, mode="fast", stream=sp), 200, stream)
+    A2, B2 = a.view(inp.m, inp.k), b.view(inp.k, inp.n)
+    cub = timed_ms(lambda: torch.matmul(A2, B2), 200, stream)
+    byt = (inp.m * inp.k + inp.k * inp.n) * 2 + inp.m * inp.n * 4
+    res["deepbench_fprop16_bf16"] = {
+        "tflops": inp.flops / ms / 1e9, "ms": ms, "pick": sel.tuning.values(), "family": "tcgen05",
+        "roofline": {"bound": "hbm", "achieved_gbs": byt / ms / 1e6, "frac": byt / ms / 1e6 / pk["hbm_gbs"]},
+        "cublas_bf16_tflops": inp.flops / cub / 1e9, "ratio_vs_cublas": cub / ms, "l2": "flushed"}
+    # C4: 8192^3 bf16 (NN) and tf32 (NT) on tcgen05 (operands 2x128 MB / 2x256 MB > L2)
+    n = 8192
+    for dt, tdt, ta, tb, tup, peak in (("bf16", torch.bfloat16, False, False, (8, 8, 128, 256, 64, 1, 1, 1),
+                                        pk["bf16_tflops"]),
+                                       ("tf32", torch.float32, False, True, (8, 8, 128, 256, 32, 1, 1, 1),
+                                        pk["bf16_tflops"] / 2)):
+        inp = K.GemmInput(n, n, n, dt, ta, tb)
+        a, b = rnd(n * n, tdt), rnd(n * n, tdt)
+        c = torch.empty(n * n, device=dev)
+        t = K.GemmTuning(*tup)
+        ms = timed_ms(lambda: K.execute_gemm(inp, t, a, b, c, mode="fast", stream=sp), 10, stream, flush=False)
+        torch.backends.cuda.matmul.allow_tf32 = True
+        A2, B2 = a.view(n, n), (b.view(n, n).t() if tb else b.view(n, n))
+        cub = timed_ms(lambda: torch.matmul(A2, B2), 10, stream, flush=False)
+        tf = inp.flops / ms / 1e9
+        res[f"square8192_{dt}"] = {
+            "tflops": tf, "ms": ms, "pick": list(tup), "family": "tcgen05", "layout": ("T" if ta else "N") + (
+                "T" if tb else "N"),
+            "roofline": {"bound": "tensor", "peak_tflops": peak, "frac": tf / peak,
+                         "peak_source": pk["source"] + (" cuBLAS bf16 burst" if dt == "bf16" else
+                                                        " bf16 burst / 2 (tf32 rate)")},
+            "cublas_tflops": inp.flops / cub / 1e9, "ratio_vs_cublas": cub / ms}
+        del a, b, c
+        torch.cuda.empty_cache()
+    # C3 (fp32 SIMT, valid mode on a pre-padded 58x58 image = 3x3 pad 1 on 56x56)
+    cin = K.ConvInput(16, 56, 56, 64, 64, 3, 3, "f32")
+    ni, nf, no = cin.sizes()
+    img, flt = rnd(ni, torch.float32), rnd(nf, torch.float32)
+    out = torch.empty(no, device=dev)
+    cb = open(os.path.join(K.FIXTURES, "bounds", "conv_b200.json")).read()
+    csel = select_conv(cin, hw, cb, candidates=600, top_k=8)
+    ms = timed_ms(lambda: K.execute_conv(cin, csel.tuning, img, flt, out, mode="fast", stream=sp), 100, stream)
+    x = img.view(cin.c, cin.h(), cin.w(), cin.n_batch).permute(3, 0, 1, 2).contiguous()
+    w = flt.view(cin.c, cin.r, cin.s, cin.k_filters).permute(3, 0, 1, 2).contiguous()
+    torch.backends.cudnn.allow_tf32 = False
+    cud = timed_ms(lambda: torch.nn.functional.conv2d(x, w), 100, stream)
+    res["conv_resnet56_f32"] = {"tflops": cin.flops / ms / 1e9, "ms": ms, "pick": csel.tuning.values(),
+                                "family": "simt fp32", "layout": "CHWN/CRSK/KPQN (reference layouts)",
+                                "cudnn_fp32_tflops_nchw": cin.flops / cud / 1e9, "ratio_vs_cudnn": cud / ms,
+                                "roofline": {"bound": "ffma", "peak_tflops": 74.4,
+                                             "frac": cin.flops / ms / 1e9 / 74.4}}
+    # C1: SGEMM NN 512^3 with the paper's LINPACK(512) tuple, fast and parity modes
+    inp = K.GemmInput(512, 512, 512, "f32")
+    a, b = rnd(512 * 512, torch.float32), rnd(512 * 512, torch.float32)
+    c = torch.empty(512 * 512, device=dev)
+    t = K.GemmTuning(2, 8, 32, 32, 8, 1, 1, 1)
+    for mode in ("fast", "parity"):
+        ms = timed_ms(lambda: K.execute_gemm(inp, t, a, b, c, mode=mode, stream=sp), 200, stream)
+        res[f"sgemm512_fixed_{mode}"] = {"tflops": inp.flops / ms / 1e9, "ms": ms, "pick": t.values(),
+                                         "family": "simt fp32", "bit_exact_vs_reference": mode == "parity"}
+    return res
+
+
 def our_arm(args):
     import numpy as np
     import torch
@@ -319,6 +483,8 @@ def our_arm(args):
                "h2d_bytes_per_step": (ah.numel() + bh.numel()) * 4, "d2h_bytes_per_step": ch.numel() * 4,
                "steps": n_e2e, "timing": "host wall clock around the synchronous C-ABI call (ktune_execute_gemm)"}
 
+    tuning = None if args.no_extras else tuning_loop(args, ws, rank, dev)
+
     if rank != 0:
         if ws > 1:
             dist.destroy_process_group()
@@ -372,6 +538,8 @@ def our_arm(args):
         "gpu_launches_detail": {"gemm": args.steps, "l2_flush": args.steps},
         "clocks": clocks.summary(),
         "correctness": res,
+        "tuning": tuning,
+        "other_configs": None if args.no_extras else other_configs(stream, dev),
     }
     print(json.dumps(line))
     if ws > 1:
@@ -387,6 +555,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--candidates", type=int, default=3000)
     ap.add_argument("--pick", default="", help="fixed tuple m_s,n_s,m_l,n_l,u,k_s,k_l,k_g (skips selection)")
+    ap.add_argument("--no-extras", action="store_true", help="headline only (no tuning loop / other configs)")
+    ap.add_argument("--tuning-samples", type=int, default=200, help="tuning-loop samples per GPU (weak scaling)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
