@@ -547,34 +547,43 @@ __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
         }
         return;
     }
-    if (tid == 0) {
-        for (int gg = 0; gg < p.nz - 1; ++gg) {
-            const unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + tile_id;
-            unsigned long long v;
-            while (true) {
-                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(flag) : "memory");
-                if (v == p.token) break;
-                __nanosleep(64);
-            }
+    for (int gg = tid; gg < p.nz - 1; gg += nthreads) {
+        const unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + tile_id;
+        unsigned long long v;
+        while (true) {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(flag) : "memory");
+            if (v == p.token) break;
+            __nanosleep(32);
         }
     }
     __syncthreads();
-    if (owner)
+    if (owner) {
+        // Fold the published partials in slice order (backends.cpp:320-325),
+        // own slice last.  All partials of one slice are loaded before any
+        // add, so a slice costs one L2 round trip rather than one per output.
+        std::int64_t idx[TILE];
+        T v[TILE];
 #pragma unroll
-        for (int i = 0; i < MS; ++i) {
-            const std::int64_t row = row0 + row_of(i);
-            if (row >= p.rows) continue;
+        for (int i = 0; i < MS; ++i)
 #pragma unroll
             for (int j = 0; j < NS; ++j) {
+                const std::int64_t row = row0 + row_of(i);
                 const std::int64_t oc = col_out[col_of(j)];
-                if (oc < 0) continue;
-                const std::int64_t idx = prob.out_index(row, oc);
-                T v = T(0);
-                for (int gg = 0; gg < p.nz - 1; ++gg)
-                    v = A::add(v, __ldcg(ws + std::int64_t(gg) * p.out_elems + idx));
-                out[idx] = A::add(v, blk[i * NS + j]);
+                idx[i * NS + j] = (row < p.rows && oc >= 0) ? prob.out_index(row, oc) : -1;
+                v[i * NS + j] = T(0);
             }
+        for (int gg = 0; gg < p.nz - 1; ++gg) {
+            const T* src = ws + std::int64_t(gg) * p.out_elems;
+            T part[TILE];
+#pragma unroll
+            for (int e = 0; e < MS * NS; ++e) part[e] = idx[e] >= 0 ? __ldcg(src + idx[e]) : T(0);
+#pragma unroll
+            for (int e = 0; e < MS * NS; ++e) v[e] = A::add(v[e], part[e]);
         }
+#pragma unroll
+        for (int e = 0; e < MS * NS; ++e)
+            if (idx[e] >= 0) out[idx[e]] = A::add(v[e], blk[e]);
+    }
 }
 
 }  // namespace ktune_dev

@@ -18,8 +18,10 @@
 //   u     BLOCK_K elements per pipeline stage (>= 32 bytes)
 //   k_g   split-K slices over the grid (deterministic ordered fix-up, as
 //         in the SIMT family)
-//   k_l, k_s, m_s, n_s  reserved for the CTA-pair / persistent variants;
-//         this build requires k_l = k_s = 1 and ignores m_s / n_s.
+//   k_s   TMEM accumulator buffers (1, or 2 = the epilogue of one tile
+//         overlaps the MMAs of the next in the persistent schedule)
+//   n_s   rasterisation width: concurrent CTAs sweep n_s column tiles
+//   k_l   reserved for CTA pairs (must be 1); m_s unused
 // Operand majors follow the GEMM layout: A K-major unless trans_a, B
 // MN-major unless trans_b (both majors are native tcgen05 descriptor modes
 // for 16-bit and tf32 inputs).
@@ -53,6 +55,9 @@ struct TcParams {
     int umma_k_bytes;             // 32 (UMMA_K elements * element size)
     int esize;
     int tmem_cols;
+    int nacc;                     // TMEM accumulator buffers (k_s)
+    int tiles_m, tiles_n;         // output tile grid
+    int raster;                   // rasterisation group width in n-tiles
     float* C;
     float* ws;
     unsigned long long* flags;
@@ -155,10 +160,47 @@ __device__ __forceinline__ bool elect_one() {
 
 constexpr int kThreads = 192;
 
+// Debug timeline (KTUNE_TC_DEBUG=<device pointer>): %globaltimer of events of
+// the CTAs with blockIdx.x = blockIdx.y = 0, 8 slots per grid slice.
+__device__ __forceinline__ void probe(const TcParams& p, int slot) {
+    if (p.dbg == nullptr || blockIdx.x != 0 || blockIdx.y != 0) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.dbg[blockIdx.z * 8 + slot] = (long long)t;
+}
+
+// Work unit u -> (tile, grid slice): slices of one tile are consecutive
+// units, so the last slice of a tile always has the largest index (the
+// ordered fold may wait on lower units only; with every CTA resident and
+// units taken in increasing order per CTA, the waits cannot deadlock).
+// Tiles are rasterised in column groups of p.raster n-tiles: the CTAs that
+// run concurrently share a few B panels and a few A panels, keeping both in
+// L2 instead of re-streaming all of B every wave.
+struct Unit {
+    int m0, n0, g, tile;
+};
+
+__device__ __forceinline__ Unit unit_of(const TcParams& p, int u) {
+    Unit w;
+    w.g = u % p.nz;
+    const int t = u / p.nz;
+    const int per_group = p.raster * p.tiles_m;
+    const int group = t / per_group;
+    const int cols = min(p.raster, p.tiles_n - group * p.raster);
+    const int local = t - group * per_group;
+    const int mt = local / cols;
+    const int nt = group * p.raster + local % cols;
+    w.m0 = mt * p.bm;
+    w.n0 = nt * p.bn;
+    w.tile = mt * p.tiles_n + nt;
+    return w;
+}
+
 template <int KIND, int KSTEPS>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                      const TcParams p) {
+    if (threadIdx.x == 0) probe(p, 0);
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-align the tile region (SW128 atoms repeat every 1024 bytes).
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
@@ -166,22 +208,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     const unsigned stage_bytes = p.a_tile_bytes + p.b_tile_bytes;
     unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + std::size_t(p.stages) * stage_bytes);
     unsigned long long* empty = full + p.stages;
-    unsigned long long* tmem_full = empty + p.stages;
-    unsigned* tmem_slot = reinterpret_cast<unsigned*>(tmem_full + 1);
+    unsigned long long* acc_full = empty + p.stages;   // [nacc] MMA -> epilogue
+    unsigned long long* acc_empty = acc_full + 2;      // [nacc] epilogue -> MMA
+    unsigned* tmem_slot = reinterpret_cast<unsigned*>(acc_empty + 2);
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
-    const int n0 = blockIdx.x * p.bn, m0 = blockIdx.y * p.bm, g = blockIdx.z;
-    const int kb_begin = g * p.kb_span;
-    const int kb_end = min(p.kb_total, kb_begin + p.kb_span);
-    const int nkb = kb_end - kb_begin;
+    const int n_units = p.tiles_m * p.tiles_n * p.nz;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(full + s, 1);
             mbar_init(empty + s, 1);
         }
-        mbar_init(tmem_full, 1);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(acc_full + a, 1);
+            mbar_init(acc_empty + a, 128);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&tma_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&tma_b)) : "memory");
@@ -195,6 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const unsigned tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) probe(p, 1);
 
     if (warp == 0) {
         // ---------------- TMA producer (whole warp loops, one lane issues) ----------------
@@ -202,135 +246,205 @@ __global__ void __launch_bounds__(kThreads, 1)
         unsigned phase = 0;
         const int a_box_elems = p.a_sw / p.esize, b_box_elems = p.b_sw / p.esize;
         const unsigned tx_bytes = p.a_boxes * p.a_box_bytes + p.b_boxes * p.b_box_bytes;
-        for (int kb = kb_begin; kb < kb_end; ++kb) {
-            mbar_wait(empty + stage, phase ^ 1u);
-            if (elect_one()) {
-                if (p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && kb - kb_begin < 64)
-                    p.dbg[2 * (kb - kb_begin)] = clock64();
-                unsigned char* sa = smem + std::size_t(stage) * stage_bytes;
-                unsigned char* sb = sa + p.a_tile_bytes;
-                mbar_expect_tx(full + stage, tx_bytes);
-                const int k0 = kb * p.bk;
-                for (int j = 0; j < p.a_boxes; ++j) {
-                    if (p.a_kmajor) tma_load_2d(sa + j * p.a_box_stride, &tma_a, full + stage, k0 + j * a_box_elems, m0);
-                    else tma_load_2d(sa + j * p.a_box_stride, &tma_a, full + stage, m0 + j * a_box_elems, k0);
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+            const Unit w = unit_of(p, u);
+            const int kb_begin = w.g * p.kb_span;
+            const int kb_end = min(p.kb_total, kb_begin + p.kb_span);
+            for (int kb = kb_begin; kb < kb_end; ++kb) {
+                mbar_wait(empty + stage, phase ^ 1u);
+                if (elect_one()) {
+                    if (kb == kb_begin && u == int(blockIdx.x)) probe(p, 2);
+                    unsigned char* sa = smem + std::size_t(stage) * stage_bytes;
+                    unsigned char* sb = sa + p.a_tile_bytes;
+                    mbar_expect_tx(full + stage, tx_bytes);
+                    const int k0 = kb * p.bk;
+                    for (int j = 0; j < p.a_boxes; ++j) {
+                        if (p.a_kmajor)
+                            tma_load_2d(sa + j * p.a_box_stride, &tma_a, full + stage, k0 + j * a_box_elems, w.m0);
+                        else
+                            tma_load_2d(sa + j * p.a_box_stride, &tma_a, full + stage, w.m0 + j * a_box_elems, k0);
+                    }
+                    for (int j = 0; j < p.b_boxes; ++j) {
+                        if (p.b_kmajor)
+                            tma_load_2d(sb + j * p.b_box_stride, &tma_b, full + stage, k0 + j * b_box_elems, w.n0);
+                        else
+                            tma_load_2d(sb + j * p.b_box_stride, &tma_b, full + stage, w.n0 + j * b_box_elems, k0);
+                    }
                 }
-                for (int j = 0; j < p.b_boxes; ++j) {
-                    if (p.b_kmajor) tma_load_2d(sb + j * p.b_box_stride, &tma_b, full + stage, k0 + j * b_box_elems, n0);
-                    else tma_load_2d(sb + j * p.b_box_stride, &tma_b, full + stage, n0 + j * b_box_elems, k0);
+                __syncwarp();
+                if (++stage == p.stages) {
+                    stage = 0;
+                    phase ^= 1u;
                 }
-            }
-            __syncwarp();
-            if (++stage == p.stages) {
-                stage = 0;
-                phase ^= 1u;
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer (whole warp loops, one lane issues) ----------------
         // Descriptors: constant high words and k-slice offsets come from the
-        // host; per k-block only the 14-bit start address changes.
+        // host; per k-block only the 14-bit start address changes.  With
+        // nacc = 2 the accumulator alternates between two TMEM column ranges,
+        // so the epilogue of one unit overlaps the MMAs of the next.
         int stage = 0;
         unsigned phase = 0;
+        int acc = 0;
+        unsigned acc_phase = 0;
         const unsigned base = smem_u32(smem);
-        for (int i = 0; i < nkb; ++i) {
-            mbar_wait(full + stage, phase);
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+            const Unit w = unit_of(p, u);
+            const int kb_begin = w.g * p.kb_span;
+            const int nkb = min(p.kb_total, kb_begin + p.kb_span) - kb_begin;
+            mbar_wait(acc_empty + acc, acc_phase ^ 1u);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            if (elect_one()) {
-                if (p.dbg && blockIdx.x == 0 && blockIdx.y == 0 && i < 64) p.dbg[2 * i + 1] = clock64();
-                const unsigned sa = base + unsigned(stage) * stage_bytes;
-                const unsigned sb = sa + p.a_tile_bytes;
+            const unsigned d_tmem = tmem_base + unsigned(acc * p.bn);
+            for (int i = 0; i < nkb; ++i) {
+                mbar_wait(full + stage, phase);
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                if (elect_one()) {
+                    if (i == 0 && u == int(blockIdx.x)) probe(p, 3);
+                    const unsigned sa = base + unsigned(stage) * stage_bytes;
+                    const unsigned sb = sa + p.a_tile_bytes;
 #pragma unroll
-                for (int kk = 0; kk < KSTEPS; ++kk) {
-                    const std::uint64_t adesc =
-                        (std::uint64_t(p.a_desc_hi) << 32) | (((sa + p.a_koff[kk]) >> 4) & 0x3FFFu) | p.a_desc_lbo;
-                    const std::uint64_t bdesc =
-                        (std::uint64_t(p.b_desc_hi) << 32) | (((sb + p.b_koff[kk]) >> 4) & 0x3FFFu) | p.b_desc_lbo;
-                    umma<KIND>(tmem_base, adesc, bdesc, p.idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                    for (int kk = 0; kk < KSTEPS; ++kk) {
+                        const std::uint64_t adesc = (std::uint64_t(p.a_desc_hi) << 32) |
+                                                    (((sa + p.a_koff[kk]) >> 4) & 0x3FFFu) | p.a_desc_lbo;
+                        const std::uint64_t bdesc = (std::uint64_t(p.b_desc_hi) << 32) |
+                                                    (((sb + p.b_koff[kk]) >> 4) & 0x3FFFu) | p.b_desc_lbo;
+                        umma<KIND>(d_tmem, adesc, bdesc, p.idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    umma_commit(empty + stage);  // slot is free once these MMAs retire
                 }
-                umma_commit(empty + stage);  // slot is free once these MMAs retire
+                __syncwarp();
+                if (++stage == p.stages) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+            if (elect_one()) {
+                if (u == int(blockIdx.x)) probe(p, 4);
+                umma_commit(acc_full + acc);
             }
             __syncwarp();
-            if (++stage == p.stages) {
-                stage = 0;
-                phase ^= 1u;
+            if (++acc == p.nacc) {
+                acc = 0;
+                acc_phase ^= 1u;
             }
         }
-        if (elect_one()) umma_commit(tmem_full);
-        __syncwarp();
     } else {
         // ---------------- epilogue (warps 2..5) ----------------
         const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-        const int row = m0 + quarter * 32 + lane;
-        const bool row_ok = row < p.M && quarter * 32 + lane < p.bm;
-        if (nkb > 0) {
-            mbar_wait(tmem_full, 0);
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        }
-        const bool last = (g == p.nz - 1);
-        const std::int64_t tiles = std::int64_t(gridDim.x) * gridDim.y;
-        const std::int64_t tile_id = std::int64_t(blockIdx.y) * gridDim.x + blockIdx.x;
         const std::int64_t MN = std::int64_t(p.M) * p.N;
-        if (last && p.nz > 1) {
-            if (threadIdx.x == 64) {
-                for (int gg = 0; gg < p.nz - 1; ++gg) {
-                    const unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + tile_id;
+        const std::int64_t tiles = std::int64_t(p.tiles_m) * p.tiles_n;
+        const int chunk = p.bn >= 32 ? 32 : 16;
+        int acc = 0;
+        unsigned acc_phase = 0;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+            const Unit w = unit_of(p, u);
+            const bool last = (w.g == p.nz - 1);
+            const int row = w.m0 + quarter * 32 + lane;
+            const bool row_ok = row < p.M && quarter * 32 + lane < p.bm;
+            mbar_wait(acc_full + acc, acc_phase);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            if (threadIdx.x == 64 && u == int(blockIdx.x)) probe(p, 5);
+            if (last && p.nz > 1) {
+                for (int gg = threadIdx.x - 64; gg < p.nz - 1; gg += 128) {
+                    const unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + w.tile;
                     unsigned long long v;
                     while (true) {
                         asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(flag) : "memory");
                         if (v == p.token) break;
-                        __nanosleep(64);
+                        __nanosleep(32);
                     }
                 }
+                asm volatile("bar.sync 1, 128;\n" ::: "memory");
+                if (threadIdx.x == 64 && u == int(blockIdx.x)) probe(p, 6);
             }
-            asm volatile("bar.sync 1, 128;\n" ::: "memory");
-        }
-        const int chunk = p.bn >= 32 ? 32 : 16;
-        for (int c0 = 0; c0 < p.bn; c0 += chunk) {
-            float v[32];
-            const unsigned taddr = tmem_base + (unsigned(quarter * 32) << 16) + unsigned(c0);
-            if (nkb > 0) {
+            for (int c0 = 0; c0 < p.bn; c0 += chunk) {
+                float v[32];
+                const unsigned taddr = tmem_base + (unsigned(quarter * 32) << 16) + unsigned(acc * p.bn + c0);
                 if (chunk == 32) tmem_ld32(taddr, v);
                 else tmem_ld16(taddr, v);
-            } else {
+                if (c0 + chunk >= p.bn) {
+                    // accumulator fully read: hand it back to the MMA warp early
+                    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(acc_empty + acc))
+                                 : "memory");
+                }
+                if (!row_ok) continue;
+                const std::int64_t base = std::int64_t(row) * p.N + w.n0 + c0;
+                const int ncols = min(chunk, p.N - (w.n0 + c0));
+                if (ncols <= 0) continue;
+                const bool vec = ncols == chunk && ((base & 3) == 0) && ((MN & 3) == 0) &&
+                                 ((reinterpret_cast<std::uintptr_t>(p.C) & 15) == 0);
+                if (p.nz == 1 || last) {
+                    if (p.nz > 1) {
+                        // ordered fold of the published partials; every partial of
+                        // one slice is loaded before any add (one L2 round trip per slice)
+                        float accv[32];
 #pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = 0.f;
-            }
-            if (!row_ok) continue;
-            const std::int64_t base = std::int64_t(row) * p.N + n0 + c0;
-            const int ncols = min(chunk, p.N - (n0 + c0));
-            if (ncols <= 0) continue;
-            if (p.nz == 1 || last) {
-                if (p.nz > 1) {
-                    for (int i = 0; i < ncols; ++i) {
-                        float acc = 0.f;
-                        for (int gg = 0; gg < p.nz - 1; ++gg) acc = __fadd_rn(acc, __ldcg(p.ws + gg * MN + base + i));
-                        v[i] = __fadd_rn(acc, v[i]);
+                        for (int i = 0; i < 32; ++i) accv[i] = 0.f;
+                        for (int gg = 0; gg < p.nz - 1; ++gg) {
+                            const float* src = p.ws + gg * MN + base;
+                            float part[32];
+                            if (vec) {
+#pragma unroll
+                                for (int i = 0; i < 32; i += 4) {
+                                    if (i < chunk) {
+                                        const float4 q = __ldcg(reinterpret_cast<const float4*>(src + i));
+                                        part[i] = q.x;
+                                        part[i + 1] = q.y;
+                                        part[i + 2] = q.z;
+                                        part[i + 3] = q.w;
+                                    }
+                                }
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) part[i] = i < ncols ? __ldcg(src + i) : 0.f;
+                            }
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) accv[i] = __fadd_rn(accv[i], part[i]);
+                        }
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = __fadd_rn(accv[i], v[i]);
+                    }
+                    float* dst = p.C + base;
+                    if (vec) {
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4)
+                            if (i < chunk)
+                                *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                    } else {
+                        for (int i = 0; i < ncols; ++i) dst[i] = v[i];
+                    }
+                } else {
+                    float* dst = p.ws + std::int64_t(w.g) * MN + base;
+                    if (vec) {
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4)
+                            if (i < chunk)
+                                __stcg(reinterpret_cast<float4*>(dst + i),
+                                       make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+                    } else {
+                        for (int i = 0; i < ncols; ++i) __stcg(dst + i, v[i]);
                     }
                 }
-                float* dst = p.C + base;
-                if (ncols == chunk && (reinterpret_cast<std::uintptr_t>(dst) & 15) == 0) {
-                    for (int i = 0; i < chunk; i += 4)
-                        *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                } else {
-                    for (int i = 0; i < ncols; ++i) dst[i] = v[i];
-                }
-            } else {
-                float* dst = p.ws + std::int64_t(g) * MN + base;
-                for (int i = 0; i < ncols; ++i) __stcg(dst + i, v[i]);
             }
-        }
-        if (!last && p.nz > 1) {
-            __threadfence();
-            asm volatile("bar.sync 1, 128;\n" ::: "memory");
-            if (threadIdx.x == 64) {
-                unsigned long long* flag = p.flags + std::int64_t(g) * tiles + tile_id;
-                asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(p.token) : "memory");
+            if (!last && p.nz > 1) {
+                __threadfence();
+                asm volatile("bar.sync 1, 128;\n" ::: "memory");
+                if (threadIdx.x == 64) {
+                    unsigned long long* flag = p.flags + std::int64_t(w.g) * tiles + w.tile;
+                    asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(p.token) : "memory");
+                }
+            }
+            if (++acc == p.nacc) {
+                acc = 0;
+                acc_phase ^= 1u;
             }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
+    if (threadIdx.x == 0) probe(p, 7);
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(p.tmem_cols));
@@ -359,6 +473,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
         return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
     }();
     return fn;
+}
+
+int num_sms() {
+    static int v = [] {
+        int dev = 0, x = 0;
+        dev::check(cudaGetDevice(&dev), "cudaGetDevice");
+        dev::check(cudaDeviceGetAttribute(&x, cudaDevAttrMultiProcessorCount, dev), "SM count");
+        return x;
+    }();
+    return v;
 }
 
 int smem_optin() {
@@ -401,8 +525,8 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
                                 std::to_string(t.m_l));
     if (t.n_l < 16 || t.n_l > 256)
         throw unsupported_error("tensor-core family: n_l must lie in [16, 256] (UMMA_N), got " + std::to_string(t.n_l));
-    if (t.k_l != 1 || t.k_s != 1)
-        throw unsupported_error("tensor-core family: k_l and k_s must be 1 in this build");
+    if (t.k_l != 1) throw unsupported_error("tensor-core family: k_l must be 1 in this build");
+    if (t.k_s > 2) throw unsupported_error("tensor-core family: k_s (TMEM accumulator buffers) must be 1 or 2");
     if (t.u * es < 32) throw unsupported_error("tensor-core family: u * element size must be >= 32 bytes");
     if (in.m > 0x7fffffff || in.n > 0x7fffffff || in.k > 0x7fffffff)
         throw unsupported_error("tensor-core family: dimensions must fit in 32 bits");
@@ -453,15 +577,18 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     p.kb_span = int(ceil_div(p.kb_total, t.k_g));
     p.nz = int(ceil_div(p.kb_total, p.kb_span));
     const std::size_t stage_bytes = std::size_t(p.a_tile_bytes) + p.b_tile_bytes;
-    const std::size_t extra = 1024 + 8 * 32 + 64;  // alignment slack + barriers + tmem slot
+    const std::size_t extra = 1024 + 8 * 32 + 64;  // alignment slack + barriers (2*stages + 4) + tmem slot
     const std::size_t optin = std::size_t(smem_optin());
     int stages = int((optin - extra) / stage_bytes);
     stages = std::min(stages, 8);
-    stages = std::min<int>(stages, std::max(2, p.kb_span));
     if (stages < 2) throw unsupported_error("tensor-core family: tile does not fit two pipeline stages in shared memory");
     p.stages = stages;
     pl.smem = extra + stage_bytes * std::size_t(stages);
-    p.tmem_cols = std::max(32, pow2_ceil(p.bn));
+    p.nacc = (t.k_s == 2 && 2 * p.bn <= 512) ? 2 : 1;
+    p.tmem_cols = std::max(32, pow2_ceil(p.nacc * p.bn));
+    p.tiles_m = int(ceil_div(in.m, p.bm));
+    p.tiles_n = int(ceil_div(in.n, p.bn));
+    p.raster = std::max(1, std::min(p.tiles_n, t.n_s));
     // instruction descriptor: F32 accumulate, operand formats, majors, N>>3, M>>4
     const unsigned fmt = in.dtype == Dtype::bf16 ? 1u : (in.dtype == Dtype::f16 ? 0u : 2u);
     p.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (unsigned(p.a_kmajor ? 0 : 1) << 15) |
@@ -489,10 +616,13 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
         p.b_koff[kk] = p.b_kmajor ? (kb / p.b_sw) * p.b_box_stride + kb % p.b_sw : (kb / es) * p.b_sw;
     }
     pl.ksteps = ksteps;
-    pl.grid = dim3(unsigned(ceil_div(in.n, p.bn)), unsigned(ceil_div(in.m, p.bm)), unsigned(p.nz));
-    if (pl.grid.y > 65535 || pl.grid.z > 65535) throw unsupported_error("grid too large for one launch");
+    // persistent grid: one CTA per SM (shared memory holds one CTA), static
+    // round-robin over (tile, slice) units
+    const std::int64_t units = std::int64_t(p.tiles_m) * p.tiles_n * p.nz;
+    if (units > 0x7fffffff) throw unsupported_error("too many work units for one launch");
+    pl.grid = dim3(unsigned(std::min<std::int64_t>(units, num_sms())), 1, 1);
     if (p.nz > 1) {
-        pl.flag_bytes = (std::size_t(pl.grid.x) * pl.grid.y * std::size_t(p.nz - 1) * 8 + 255) / 256 * 256;
+        pl.flag_bytes = (std::size_t(p.tiles_m) * p.tiles_n * std::size_t(p.nz - 1) * 8 + 255) / 256 * 256;
         pl.ws_bytes = pl.flag_bytes + std::size_t(p.nz - 1) * std::size_t(in.m) * std::size_t(in.n) * 4;
     }
     return pl;
