@@ -335,7 +335,10 @@ std::size_t gemm_workspace_bytes(const GemmInput& in, const GemmTuning& t) {
     return gemm_plan(in, t).ws_bytes;
 }
 
-std::size_t conv_workspace_bytes(const ConvInput& in, const ConvTuning& t) { return conv_plan(in, t).ws_bytes; }
+std::size_t conv_workspace_bytes(const ConvInput& in, const ConvTuning& t) {
+    if (is_tensor_core_dtype(in.dtype)) return umma::conv_workspace_bytes(in, t);
+    return conv_plan(in, t).ws_bytes;
+}
 
 void gemm(const GemmInput& in, const GemmTuning& t, Mode mode, const void* a, const void* b, void* c, void* ws,
           std::size_t ws_bytes, cudaStream_t stream) {
@@ -351,6 +354,10 @@ void gemm(const GemmInput& in, const GemmTuning& t, Mode mode, const void* a, co
 
 void conv(const ConvInput& in, const ConvTuning& t, Mode mode, const void* images, const void* filters, void* outputs,
           void* ws, std::size_t ws_bytes, cudaStream_t stream) {
+    if (is_tensor_core_dtype(in.dtype)) {
+        umma::conv(in, t, images, filters, outputs, ws, ws_bytes, stream);
+        return;
+    }
     Plan pl = conv_plan(in, t, images, filters);
     bind_workspace(pl, ws, ws_bytes);
     if (in.dtype == Dtype::f32) launch_conv_t<float>(in, t, pl, mode, images, filters, outputs, stream);
@@ -365,6 +372,7 @@ LaunchInfo gemm_launch_info(const GemmInput& in, const GemmTuning& t, Mode mode)
 }
 
 LaunchInfo conv_launch_info(const ConvInput& in, const ConvTuning& t, Mode mode) {
+    if (is_tensor_core_dtype(in.dtype)) return umma::conv_launch_info(in, t);
     Plan pl = conv_plan(in, t);
     pick(true, in.dtype, mode, pl);
     return LaunchInfo{pl.threads, pl.smem, int(pl.grid.x), int(pl.grid.y), int(pl.grid.z), pl.generic, "simt"};

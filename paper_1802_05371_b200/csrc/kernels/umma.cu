@@ -36,6 +36,7 @@
 #include <string>
 
 #include "umma.hpp"
+#include "umma_common.cuh"
 
 namespace ktune_dev {
 namespace tc {
@@ -68,95 +69,6 @@ struct TcParams {
     long long* dbg;  // optional timeline probe (CTA 0): [kb][0]=producer issue, [kb][1]=mma start
 };
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, unsigned long long* bar, int c0,
-                                            int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::
-            "r"(smem_u32(dst)),
-        "l"(reinterpret_cast<std::uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-        : "memory");
-}
-
-template <int KIND>
-__device__ __forceinline__ void umma(unsigned tmem_d, std::uint64_t adesc, std::uint64_t bdesc, unsigned idesc,
-                                     unsigned accumulate) {
-    if constexpr (KIND == 0) {
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-    } else {
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-    }
-}
-
-__device__ __forceinline__ void umma_commit(unsigned long long* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld32(unsigned taddr, float* v) {
-    unsigned r[32];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
-        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ void tmem_ld16(unsigned taddr, float* v) {
-    unsigned r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ bool elect_one() {
-    unsigned pred = 0;
-    asm volatile(
-        "{\n.reg .b32 rx;\n.reg .pred px;\nelect.sync rx|px, 0xffffffff;\nselp.u32 %0, 1, 0, px;\n}\n"
-        : "=r"(pred));
-    return pred != 0;
-}
 
 constexpr int kThreads = 192;
 
@@ -461,39 +373,7 @@ namespace {
 
 using ktune_dev::tc::TcParams;
 
-std::int64_t ceil_div(std::int64_t a, std::int64_t b) { return (a + b - 1) / b; }
-
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q{};
-        dev::check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q),
-                   "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
-        if (p == nullptr || q != cudaDriverEntryPointSuccess) throw cuda_error("cuTensorMapEncodeTiled unavailable");
-        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }();
-    return fn;
-}
-
-int num_sms() {
-    static int v = [] {
-        int dev = 0, x = 0;
-        dev::check(cudaGetDevice(&dev), "cudaGetDevice");
-        dev::check(cudaDeviceGetAttribute(&x, cudaDevAttrMultiProcessorCount, dev), "SM count");
-        return x;
-    }();
-    return v;
-}
-
-int smem_optin() {
-    static int v = [] {
-        int dev = 0, x = 0;
-        dev::check(cudaGetDevice(&dev), "cudaGetDevice");
-        dev::check(cudaDeviceGetAttribute(&x, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "smem attr");
-        return x;
-    }();
-    return v;
-}
+using namespace detail;
 
 struct TcPlan {
     TcParams p{};
@@ -504,11 +384,6 @@ struct TcPlan {
     int ksteps{4};
 };
 
-int pow2_ceil(int x) {
-    int v = 1;
-    while (v < x) v <<= 1;
-    return v;
-}
 
 TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     in.validate();
@@ -628,45 +503,6 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     return pl;
 }
 
-CUtensorMapDataType tma_dtype(Dtype d) {
-    switch (d) {
-        case Dtype::bf16: return CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-        case Dtype::f16: return CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-        default: return CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-    }
-}
-
-CUtensorMapSwizzle tma_swizzle(int sw) {
-    return sw == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : (sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
-}
-
-// 2-D map over a row-major [outer][inner] matrix; box = {box_inner, box_outer}.
-CUtensorMap make_map(const void* base, Dtype dt, std::int64_t inner, std::int64_t outer, int box_inner, int box_outer,
-                     int sw) {
-    CUtensorMap m;
-    const int es = dtype_size_bytes(dt);
-    cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
-    cuuint64_t strides[1] = {cuuint64_t(inner) * cuuint64_t(es)};
-    cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_outer)};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode_fn()(&m, tma_dtype(dt), 2, const_cast<void*>(base), dims, strides, box, estr,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, tma_swizzle(sw), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
-    return m;
-}
-
-unsigned long long next_token() {
-    static std::mutex mu;
-    static unsigned long long state = 0x243f6a8885a308d3ULL ^ reinterpret_cast<std::uintptr_t>(&mu);
-    std::lock_guard<std::mutex> lock(mu);
-    state += 0x9e3779b97f4a7c15ULL;
-    unsigned long long x = state;
-    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
-    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
-    x ^= x >> 31;
-    return x ? x : 1;
-}
 
 }  // namespace
 

@@ -14,5 +14,11 @@ void gemm(const GemmInput& in, const GemmTuning& t, const void* a, const void* b
           std::size_t ws_bytes, cudaStream_t stream);
 dev::LaunchInfo gemm_launch_info(const GemmInput& in, const GemmTuning& t);
 
+// K4c: implicit-GEMM convolution (bf16 / f16), see umma_conv.cu.
+std::size_t conv_workspace_bytes(const ConvInput& in, const ConvTuning& t);
+void conv(const ConvInput& in, const ConvTuning& t, const void* images, const void* filters, void* outputs, void* ws,
+          std::size_t ws_bytes, cudaStream_t stream);
+dev::LaunchInfo conv_launch_info(const ConvInput& in, const ConvTuning& t);
+
 }  // namespace umma
 }  // namespace ktune
