@@ -18,6 +18,7 @@
 #include <chrono>
 #include <random>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -103,7 +104,18 @@ std::int64_t slice_gcd_span(std::int64_t red, std::int64_t kg_span, int nz, int 
     return g;
 }
 
-constexpr std::size_t kStageBudget = 48 * 1024;  // smem the pipeline aims to fill
+constexpr std::size_t kStageBudget = 48 * 1024;        // smem the pipeline fills at least
+constexpr std::size_t kSmemPerSm = 220 * 1024;          // usable per SM, less per-block reserve
+
+int device_sm_count() {
+    static int value = [] {
+        int dev = 0, v = 0;
+        check(cudaGetDevice(&dev), "cudaGetDevice");
+        check(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev), "SM count");
+        return v;
+    }();
+    return value;
+}
 
 // rows/red/out: problem extents; ml,nl,ms,ns,ks,kl,kg,u: mapped tuple;
 // arm/brm: operand staging layouts; va/vb: vector widths (elements).
@@ -154,7 +166,14 @@ Plan plan_simt(std::int64_t rows, std::int64_t red, std::int64_t out_elems, std:
     pl.grid = dim3(unsigned(pl.col_tiles), unsigned(pl.row_tiles), unsigned(p.nz));
     const std::size_t stage_bytes = std::size_t(p.a_stage + p.b_stage) * std::size_t(esize);
     const std::int64_t nsteps = ceil_div(ceil_div(p.kg_span, kl), p.w);
-    p.stages = int(std::clamp<std::size_t>(kStageBudget / stage_bytes, 2, 6));
+    // Pipeline depth: as deep as shared memory allows while every block of
+    // the grid stays resident in one wave (a block that waits for a free slot
+    // pays the whole pipeline latency again), at least kStageBudget worth.
+    const std::int64_t blocks = std::int64_t(pl.col_tiles) * pl.row_tiles * p.nz;
+    const std::int64_t per_sm = std::max<std::int64_t>(1, ceil_div(blocks, device_sm_count()));
+    std::size_t budget = std::max<std::size_t>(kStageBudget, kSmemPerSm / std::size_t(per_sm));
+    if (const char* e = std::getenv("KTUNE_SIMT_STAGE_BYTES")) budget = std::size_t(std::strtoull(e, nullptr, 0));
+    p.stages = int(std::clamp<std::size_t>(budget / stage_bytes, 2, 8));
     p.stages = int(std::max<std::int64_t>(2, std::min<std::int64_t>(p.stages, nsteps + 1)));
     const std::size_t red_tile = std::size_t(ml) * nl * std::size_t(esize);
     const std::size_t head = std::size_t(2) * nl * sizeof(std::int64_t);
@@ -179,9 +198,14 @@ Plan plan_simt(std::int64_t rows, std::int64_t red, std::int64_t out_elems, std:
 
 using Lookup = const void* (*)(int, int, int);
 
-Lookup gemm_lookup(Dtype dt, bool par, bool arm, bool brm) {
+Lookup gemm_lookup(Dtype dt, bool par, bool arm, bool brm, bool narrow) {
     using namespace ktune_dev;
     const int lay = (arm ? 0 : 1) + (brm ? 2 : 0);  // nn, tn, nt, tt
+    static const Lookup f32pn[] = {&simt_gemm_f32_parity_narrow_nn, &simt_gemm_f32_parity_narrow_tn,
+                                   &simt_gemm_f32_parity_narrow_nt, &simt_gemm_f32_parity_narrow_tt};
+    static const Lookup f32fn[] = {&simt_gemm_f32_fast_narrow_nn, &simt_gemm_f32_fast_narrow_tn,
+                                   &simt_gemm_f32_fast_narrow_nt, &simt_gemm_f32_fast_narrow_tt};
+    if (narrow && dt == Dtype::f32) return par ? f32pn[lay] : f32fn[lay];
     static const Lookup f32p[] = {&simt_gemm_f32_parity_nn, &simt_gemm_f32_parity_tn, &simt_gemm_f32_parity_nt,
                                   &simt_gemm_f32_parity_tt};
     static const Lookup f32f[] = {&simt_gemm_f32_fast_nn, &simt_gemm_f32_fast_tn, &simt_gemm_f32_fast_nt,
@@ -197,8 +221,14 @@ Lookup gemm_lookup(Dtype dt, bool par, bool arm, bool brm) {
 const void* pick(bool conv, Dtype dt, Mode mode, Plan& pl) {
     using namespace ktune_dev;
     const bool par = (mode == Mode::parity);
+    // <= 256 threads: the 255-register NARROW instantiation when one exists
+    if (!pl.generic && pl.threads <= kNarrowThreads && dt == Dtype::f32) {
+        const void* k = conv ? (par ? simt_conv_f32_parity_narrow : simt_conv_f32_fast_narrow)(pl.ms, pl.ns, pl.ks)
+                             : gemm_lookup(dt, par, pl.arm, pl.brm, true)(pl.ms, pl.ns, pl.ks);
+        if (k != nullptr) return k;
+    }
     Lookup fn;
-    if (!conv) fn = gemm_lookup(dt, par, pl.arm, pl.brm);
+    if (!conv) fn = gemm_lookup(dt, par, pl.arm, pl.brm, false);
     else if (dt == Dtype::f32) fn = par ? &simt_conv_f32_parity : &simt_conv_f32_fast;
     else fn = par ? &simt_conv_f64_parity : &simt_conv_f64_fast;
     const void* k = pl.generic ? nullptr : fn(pl.ms, pl.ns, pl.ks);
@@ -220,6 +250,10 @@ void prepare(const void* kernel, std::size_t smem) {
     if (it != configured.end() && it->second >= smem) return;
     check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(std::max<std::size_t>(smem, 48 * 1024))),
           "cudaFuncSetAttribute(smem)");
+    // Every kernel of this library runs with the max-shared L1 carveout, so
+    // consecutive launches never pay an SM L1/shared reconfiguration.
+    check(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared),
+          "cudaFuncSetAttribute(carveout)");
     configured[kernel] = std::max<std::size_t>(smem, 48 * 1024);
 }
 
@@ -266,8 +300,19 @@ Plan gemm_plan(const GemmInput& in, const GemmTuning& t, const void* a = nullptr
     auto vb = [&](int w, std::int64_t span_gcd) {
         return brm ? vec_width(es, {in.k, span_gcd}, {b}, w) : vec_width(es, {in.n}, {b}, t.n_l);
     };
-    return plan_simt(in.m, in.k, in.m * in.n, ceil_div(in.n, t.n_l), t.m_l, t.n_l, t.m_s, t.n_s, t.k_s, t.k_l, t.k_g,
-                     t.u, es, arm, brm, va, vb);
+    Plan pl = plan_simt(in.m, in.k, in.m * in.n, ceil_div(in.n, t.n_l), t.m_l, t.n_l, t.m_s, t.n_s, t.k_s, t.k_l,
+                        t.k_g, t.u, es, arm, brm, va, vb);
+    // Precomputed chunk loader: every thread's chunks fit ktune_dev::kChunkMax
+    // and every operand offset fits in 32 bits.
+    auto chunks = [&](int lrows, int lv) {
+        const std::int64_t total = std::int64_t(pl.p.kl) << (lrows + pl.p.lw - lv);
+        return ceil_div(total, pl.threads);
+    };
+    const std::int64_t lim = std::int64_t(1) << 31;
+    pl.p.fast_ld = chunks(pl.p.lml, pl.p.lva) <= ktune_dev::kChunkMax &&
+                   chunks(pl.p.lnl, pl.p.lvb) <= ktune_dev::kChunkMax && in.m * in.k < lim && in.k * in.n < lim &&
+                   in.k + t.u < lim;
+    return pl;
 }
 
 Plan conv_plan(const ConvInput& in, const ConvTuning& t, const void* img = nullptr, const void* flt = nullptr) {
@@ -295,6 +340,7 @@ void launch_gemm_t(const GemmInput& in, Plan& pl, Mode mode, const void* a, cons
     ktune_dev::GemmProblem<T> prob{static_cast<const T*>(a), static_cast<const T*>(b), in.m, in.n, in.k,
                                    in.trans_a ? 1 : 0, in.trans_b ? 1 : 0, pl.p.nl};
     pl.p.out = c;
+    if (const char* d = std::getenv("KTUNE_SIMT_DEBUG")) pl.p.dbg = reinterpret_cast<long long*>(std::strtoull(d, nullptr, 0));
     const void* k = pick(false, in.dtype, mode, pl);
     prepare(k, pl.smem);
     void* args[] = {&prob, &pl.p};
@@ -390,6 +436,17 @@ __global__ void flush_kernel(uint4* buf, std::size_t n16, unsigned salt) {
         buf[i] = make_uint4(salt, unsigned(i), salt ^ 0x9e3779b9u, unsigned(i >> 32));
 }
 
+// Reads the first half of the flush buffer (leaves L2 holding clean lines).
+__global__ void read_sweep_kernel(const uint4* buf, std::size_t n16, uint4* sink) {
+    const std::size_t stride = std::size_t(gridDim.x) * blockDim.x;
+    unsigned acc = 0;
+    for (std::size_t i = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16; i += stride) {
+        const uint4 v = __ldcg(buf + i);
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    if (acc == 0x12345679u) sink->x = acc;
+}
+
 // splitmix64-derived uniform [0,1) with 53 (f64) / 24 (f32) random bits.
 __device__ __forceinline__ std::uint64_t mix64(std::uint64_t x) {
     x += 0x9e3779b97f4a7c15ULL;
@@ -451,8 +508,26 @@ void l2_flush(cudaStream_t stream) {
     }
     int sms = 0;
     check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
+    static const bool carveout = [] {
+        // same carveout as the measured kernels: the flush must not leave the
+        // SMs in an L1-heavy configuration that the next launch pays to undo
+        check(cudaFuncSetAttribute(reinterpret_cast<const void*>(&flush_kernel),
+                                   cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared),
+              "flush carveout");
+        check(cudaFuncSetAttribute(reinterpret_cast<const void*>(&read_sweep_kernel),
+                                   cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared),
+              "flush carveout");
+        return true;
+    }();
+    (void)carveout;
     flush_kernel<<<sms * 4, 512, 0, stream>>>(static_cast<uint4*>(fb->ptr), fb->bytes / 16, fb->salt);
     check(cudaGetLastError(), "flush launch");
+    static const bool rw = std::getenv("KTUNE_FLUSH_RW") != nullptr;
+    if (rw) {
+        read_sweep_kernel<<<sms * 4, 512, 0, stream>>>(static_cast<const uint4*>(fb->ptr), fb->bytes / 16 / 2,
+                                                       static_cast<uint4*>(fb->ptr) + fb->bytes / 16 - 1);
+        check(cudaGetLastError(), "flush read launch");
+    }
 }
 
 void fill_uniform(void* dst, std::int64_t n, Dtype dtype, std::uint64_t seed, cudaStream_t stream) {

@@ -57,11 +57,34 @@ struct SimtParams {
     void* ws;               // k_g partials [nz-1][out_elems]
     unsigned long long* flags;  // [nz-1][tiles] publication tokens
     unsigned long long token;   // unique per launch (never 0)
+    int fast_ld;                // affine problems: per-thread chunk state precomputed (see ChunkLd)
+    long long* dbg;             // optional timeline probe (KTUNE_SIMT_DEBUG): blocks x = 0, y in {0, 1}
+};
+
+__device__ __forceinline__ void simt_probe(const SimtParams& p, int slot) {
+    if (p.dbg == nullptr || blockIdx.x != 0 || blockIdx.y > 1 || threadIdx.x != 0) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.dbg[(blockIdx.y * gridDim.z + blockIdx.z) * 8 + slot] = (long long)t;
+}
+
+// Per-thread cp.async chunks of one operand, precomputed once per block for
+// problems whose addresses are affine in the reduction index (GEMM): element
+// offset at the block's first step, smem destination, remaining reduction
+// columns and valid lanes.  A step then costs a few integer ops per chunk
+// instead of the full index decomposition.
+constexpr int kChunkMax = 4;
+struct ChunkLd {
+    int off;  // element offset of the chunk at step 0 (operand < 2^31 elements)
+    int dst;  // element offset inside one stage
+    int lim;  // reduction columns left in the group from the chunk's first column
+    int cnt;  // valid elements along the contiguous dimension (0 = chunk outside the tensor)
 };
 
 // ---- GEMM policy: A is M x K (K x M when ta), B is K x N (N x K when tb) ----
 template <typename T>
 struct GemmProblem {
+    static constexpr bool kAffine = true;
     const T* a;
     const T* b;
     std::int64_t M, N, K;
@@ -86,6 +109,9 @@ struct GemmProblem {
         out_col = base;
     }
     __device__ std::int64_t out_index(std::int64_t row, std::int64_t out_col) const { return row * N + out_col; }
+    // element distance of one reduction step along each operand
+    __device__ std::int64_t a_kstride() const { return ta ? M : 1; }
+    __device__ std::int64_t b_kstride() const { return tb ? 1 : N; }
 };
 
 // ---- CONV policy: images C,H,W,N; filters C,R,S,K; outputs K,P,Q,N --------
@@ -94,6 +120,7 @@ struct GemmProblem {
 // with off(t) the indirection-table offset of backends.cpp:197-216.
 template <typename T>
 struct ConvProblem {
+    static constexpr bool kAffine = false;
     const T* flt;
     const T* img;
     std::int64_t Nb, P, Q, K, C, R, S, H, W;
@@ -205,8 +232,14 @@ struct LaunchCap {
 // BRM: the B tile is staged [col][kk] (GEMM transposed B); otherwise [kk][col].
 // Each operand is copied with cp.async chunks of 2^lv elements along its
 // global contiguous dimension, so smem keeps that dimension contiguous.
-template <class Prob, typename T, int MS_, int NS_, int KS_, bool PARITY, bool ARM, bool BRM>
-__global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
+// NARROW instantiations are bounded at 256 threads per block, which lifts the
+// register cap from 64 to 255 for small register tiles (software-pipelined
+// shared-memory reads, no spills in the k_g fold); the host picks them
+// whenever the tuple needs <= 256 threads.
+constexpr int kNarrowThreads = 256;
+
+template <class Prob, typename T, int MS_, int NS_, int KS_, bool PARITY, bool ARM, bool BRM, bool NARROW = false>
+__global__ void __launch_bounds__(NARROW ? kNarrowThreads : LaunchCap<MS_, NS_, KS_>::threads)
     simt_kernel(const Prob prob, const SimtParams p) {
     constexpr bool RT = (MS_ == 0);  // runtime-tile generic kernel
     const int MS = RT ? p.ms : MS_;
@@ -239,6 +272,7 @@ __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
     const std::int64_t kl_span = (s_hi - s_lo + p.kl - 1) / p.kl;
     const std::int64_t nsteps = (kl_span + p.w - 1) / p.w;
 
+    simt_probe(p, 0);
     for (int x = tid; x < p.nl; x += nthreads) prob.column(ct, x, col_base[x], col_out[x]);
     __syncthreads();
 
@@ -291,8 +325,111 @@ __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
             cp_async_zfill<BYTES>(d, src, n * int(sizeof(T)));
         }
     };
+    // ---- precomputed chunk state (affine problems, host-checked envelope) ----
+    ChunkLd ca[kChunkMax], cb[kChunkMax];
+    int nca = 0, ncb = 0;
+    std::int64_t a_wk = 0, b_wk = 0;  // element advance of one step
+    if constexpr (Prob::kAffine) {
+        if (p.fast_ld) {
+            a_wk = std::int64_t(p.w) * prob.a_kstride();
+            b_wk = std::int64_t(p.w) * prob.b_kstride();
+            {
+                const int VA = 1 << p.lva;
+                const int lchunks = p.lml + p.lw - p.lva;
+                const int total = p.kl << lchunks;
+                const int inner = ARM ? (p.lw - p.lva) : (p.lml - p.lva);
+                nca = min(kChunkMax, max(0, (total - tid + nthreads - 1) / nthreads));
+#pragma unroll
+                for (int i = 0; i < kChunkMax; ++i) {
+                    if (i >= nca) break;
+                    const int e = tid + i * nthreads;
+                    const int gx = e >> lchunks;
+                    const int c = e & ((1 << lchunks) - 1);
+                    const int outer = c >> inner;
+                    const int in = (c & ((1 << inner) - 1)) << p.lva;
+                    const int ii = ARM ? outer : in;
+                    const int kk = ARM ? in : outer;
+                    const std::int64_t glo = min(s_hi, s_lo + gx * kl_span);
+                    const std::int64_t ghi = min(s_hi, glo + kl_span);
+                    const std::int64_t t0 = glo + kk;
+                    const std::int64_t row = row0 + ii;
+                    const bool rv = row < p.rows;
+                    ca[i].off = rv ? int(prob.a_addr(row, t0) - prob.a) : 0;
+                    ca[i].dst = gx * p.a_group + (ARM ? ii * p.a_ld + kk : kk * p.a_ld + ii);
+                    ca[i].lim = int(ghi - t0);
+                    ca[i].cnt = ARM ? (rv ? VA : 0) : int(max(std::int64_t(0), min(std::int64_t(VA), p.rows - row)));
+                }
+            }
+            {
+                const int VB = 1 << p.lvb;
+                const int lchunks = p.lnl + p.lw - p.lvb;
+                const int total = p.kl << lchunks;
+                const int inner = BRM ? (p.lw - p.lvb) : (p.lnl - p.lvb);
+                ncb = min(kChunkMax, max(0, (total - tid + nthreads - 1) / nthreads));
+#pragma unroll
+                for (int i = 0; i < kChunkMax; ++i) {
+                    if (i >= ncb) break;
+                    const int e = tid + i * nthreads;
+                    const int gx = e >> lchunks;
+                    const int c = e & ((1 << lchunks) - 1);
+                    const int outer = c >> inner;
+                    const int in = (c & ((1 << inner) - 1)) << p.lvb;
+                    const int xx = BRM ? outer : in;
+                    const int kk = BRM ? in : outer;
+                    const std::int64_t glo = min(s_hi, s_lo + gx * kl_span);
+                    const std::int64_t ghi = min(s_hi, glo + kl_span);
+                    const std::int64_t t0 = glo + kk;
+                    const std::int64_t base = col_base[xx];
+                    cb[i].off = base >= 0 ? int(prob.b_addr(t0, base) - prob.b) : 0;
+                    cb[i].dst = gx * p.b_group + (BRM ? xx * p.b_ld + kk : kk * p.b_ld + xx);
+                    cb[i].lim = int(ghi - t0);
+                    cb[i].cnt = BRM ? (base >= 0 ? VB : 0) : prob.b_cols_valid(base, VB);
+                }
+            }
+        }
+    }
+    auto load_fast = [&]<int BA, int BB>(std::int64_t st, T* dst) {
+        if constexpr (Prob::kAffine) {
+            const int dk = int(st) * p.w;
+            const T* dummy = reinterpret_cast<const T*>(p.out);
+#pragma unroll
+            for (int i = 0; i < kChunkMax; ++i) {
+                if (i < nca) {
+                    const int r = ca[i].lim - dk;
+                    const int n = ARM ? min(max(r, 0), ca[i].cnt) : (r > 0 ? ca[i].cnt : 0);
+                    const T* src = n > 0 ? prob.a + (ca[i].off + st * a_wk) : dummy;
+                    cp_async_zfill<BA>(dst + ca[i].dst, src, n * int(sizeof(T)));
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < kChunkMax; ++i) {
+                if (i < ncb) {
+                    const int r = cb[i].lim - dk;
+                    const int n = BRM ? min(max(r, 0), cb[i].cnt) : (r > 0 ? cb[i].cnt : 0);
+                    const T* src = n > 0 ? prob.b + (cb[i].off + st * b_wk) : dummy;
+                    cp_async_zfill<BB>(dst + p.a_stage + cb[i].dst, src, n * int(sizeof(T)));
+                }
+            }
+        }
+    };
     auto load_stage = [&](std::int64_t st, int slot) {
         T* dst = stage_mem + slot * stage_elems;
+        if constexpr (Prob::kAffine) {
+            if (p.fast_ld) {
+                constexpr int E = int(sizeof(T));
+                const int ba = E << p.lva, bb = E << p.lvb;
+                if (ba == 16 && bb == 16) load_fast.template operator()<16, 16>(st, dst);
+                else if (ba == 16 && bb == E) load_fast.template operator()<16, E>(st, dst);
+                else if (ba == E && bb == 16) load_fast.template operator()<E, 16>(st, dst);
+                else if (ba == 16 && bb == 8) load_fast.template operator()<16, 8>(st, dst);
+                else if (ba == 8 && bb == 16) load_fast.template operator()<8, 16>(st, dst);
+                else if (ba == 8 && bb == 8) load_fast.template operator()<8, 8>(st, dst);
+                else if (ba == 8 && bb == E) load_fast.template operator()<8, E>(st, dst);
+                else if (ba == E && bb == 8) load_fast.template operator()<E, 8>(st, dst);
+                else load_fast.template operator()<E, E>(st, dst);
+                return;
+            }
+        }
         switch (int(sizeof(T)) << p.lva) {
             case 16: load_a.template operator()<16>(st, dst); break;
             case 8: load_a.template operator()<8>(st, dst); break;
@@ -335,6 +472,7 @@ __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
     // vector path needs VK | w and k_s | VK (set = c % k_s inside a chunk)
     const bool kvec = (KS_ > 0 && KS_ <= VK) && (p.w % VK) == 0;
     int slot = 0;
+    simt_probe(p, 1);
     for (std::int64_t st = 0; st < nsteps; ++st) {
         cp_async_wait_dyn(S - 2);
         __syncthreads();
@@ -475,10 +613,12 @@ __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
                 }
             }
         }
+        if (st == 0) simt_probe(p, 2);
         if (++slot == S) slot = 0;
     }
     cp_async_wait<0>();
     __syncthreads();
+    simt_probe(p, 3);
 
     // ---- fold: k_s sets within a thread, then k_l groups in order ----------
     // (backends.cpp:311-318): blk = ((0 + g0s0) + g0s1) + ... + g1s0 + ...
@@ -503,6 +643,7 @@ __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
         __syncthreads();
     }
 
+    simt_probe(p, 4);
     // ---- output: direct store, or k_g partial + last-block ordered merge ---
     const bool owner = (lg == p.kl - 1);
     T* out = static_cast<T*>(p.out);
@@ -539,12 +680,16 @@ __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
                     if (oc >= 0) __stcg(ws + std::int64_t(g) * p.out_elems + prob.out_index(row, oc), blk[i * NS + j]);
                 }
             }
-        __threadfence();
+        // bar.sync orders every thread's partial stores before thread 0's
+        // release; a gpu-scope release is cumulative over them (PTX memory
+        // model), so no per-thread fence is needed.
         __syncthreads();
         if (tid == 0) {
             unsigned long long* flag = p.flags + std::int64_t(g) * tiles + tile_id;
-            asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(p.token) : "memory");
+            asm volatile("fence.acq_rel.gpu;\nst.release.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(p.token)
+                         : "memory");
         }
+        simt_probe(p, 5);
         return;
     }
     for (int gg = tid; gg < p.nz - 1; gg += nthreads) {
@@ -557,6 +702,7 @@ __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
         }
     }
     __syncthreads();
+    simt_probe(p, 6);
     if (owner) {
         // Fold the published partials in slice order (backends.cpp:320-325),
         // own slice last.  All partials of one slice are loaded before any
@@ -572,18 +718,30 @@ __global__ void __launch_bounds__(LaunchCap<MS_, NS_, KS_>::threads)
                 idx[i * NS + j] = (row < p.rows && oc >= 0) ? prob.out_index(row, oc) : -1;
                 v[i * NS + j] = T(0);
             }
-        for (int gg = 0; gg < p.nz - 1; ++gg) {
-            const T* src = ws + std::int64_t(gg) * p.out_elems;
-            T part[TILE];
+        // Batches of FB slices: FB*TILE independent L2 loads in flight, then
+        // the adds in slice order (the order is what parity fixes, not the loads).
+        constexpr int FB = TILE >= 32 ? 1 : 32 / TILE;
+        for (int g0 = 0; g0 < p.nz - 1; g0 += FB) {
+            T part[FB][TILE];
 #pragma unroll
-            for (int e = 0; e < MS * NS; ++e) part[e] = idx[e] >= 0 ? __ldcg(src + idx[e]) : T(0);
+            for (int f = 0; f < FB; ++f) {
+                const T* src = ws + std::int64_t(g0 + f) * p.out_elems;
+                const bool live = g0 + f < p.nz - 1;
 #pragma unroll
-            for (int e = 0; e < MS * NS; ++e) v[e] = A::add(v[e], part[e]);
+                for (int e = 0; e < MS * NS; ++e) part[f][e] = (live && idx[e] >= 0) ? __ldcg(src + idx[e]) : T(0);
+            }
+#pragma unroll
+            for (int f = 0; f < FB; ++f)
+                if (g0 + f < p.nz - 1)
+#pragma unroll
+                    for (int e = 0; e < MS * NS; ++e) v[e] = A::add(v[e], part[f][e]);
         }
 #pragma unroll
         for (int e = 0; e < MS * NS; ++e)
             if (idx[e] >= 0) out[idx[e]] = A::add(v[e], blk[e]);
     }
+    __syncthreads();
+    simt_probe(p, 7);
 }
 
 }  // namespace ktune_dev

@@ -21,6 +21,21 @@
 
 #define KTUNE_CONV_TILES(X) KTUNE_CONV_TILES_CS(X, 1) X(8, 16, 1) KTUNE_CONV_TILES_CS(X, 2)
 
+// NARROW (<= 256 threads, up to 255 registers) variants: the tiles whose wide
+// instantiation is register-capped below 255 (accumulators <= 32).
+#define KTUNE_GEMM_TILES_NARROW_KS(X, KS) \
+    X(1, 1, KS) X(1, 2, KS) X(2, 1, KS) X(1, 4, KS) X(2, 2, KS) X(4, 1, KS) X(1, 8, KS) X(2, 4, KS) X(4, 2, KS) \
+    X(8, 1, KS)
+#define KTUNE_GEMM_TILES_NARROW(X)                                                                        \
+    KTUNE_GEMM_TILES_NARROW_KS(X, 1) KTUNE_GEMM_TILES_NARROW_KS(X, 2) X(2, 8, 1) X(4, 4, 1) X(8, 2, 1) \
+    X(4, 8, 1) X(8, 4, 1) X(1, 1, 4) X(1, 2, 4) X(2, 1, 4) X(1, 4, 4) X(2, 2, 4) X(4, 1, 4) X(1, 8, 4) X(2, 4, 4) \
+    X(4, 2, 4) X(8, 1, 4) X(2, 8, 2) X(4, 4, 2) X(8, 2, 2)
+#define KTUNE_CONV_TILES_NARROW(X)                                                                                \
+    X(1, 1, 1) X(1, 2, 1) X(1, 4, 1) X(1, 8, 1) X(1, 16, 1) X(2, 1, 1) X(2, 2, 1) X(2, 4, 1) X(2, 8, 1) X(2, 16, 1) \
+    X(4, 1, 1) X(4, 2, 1) X(4, 4, 1) X(4, 8, 1) X(8, 1, 1) X(8, 2, 1) X(8, 4, 1) X(1, 1, 2) X(1, 2, 2) X(1, 4, 2)  \
+    X(1, 8, 2) X(1, 16, 2) X(2, 1, 2) X(2, 2, 2) X(2, 4, 2) X(2, 8, 2) X(4, 1, 2) X(4, 2, 2) X(4, 4, 2) X(8, 1, 2) \
+    X(8, 2, 2)
+
 namespace ktune_dev {
 
 // Kernel pointer lookup per (kind, dtype, mode); defined in
@@ -40,6 +55,10 @@ KTUNE_DECLARE_LOOKUP(conv, f32, parity)
 KTUNE_DECLARE_LOOKUP(conv, f32, fast)
 KTUNE_DECLARE_LOOKUP(conv, f64, parity)
 KTUNE_DECLARE_LOOKUP(conv, f64, fast)
+KTUNE_DECLARE_GEMM_LOOKUPS(f32, parity_narrow)
+KTUNE_DECLARE_GEMM_LOOKUPS(f32, fast_narrow)
+KTUNE_DECLARE_LOOKUP(conv, f32, parity_narrow)
+KTUNE_DECLARE_LOOKUP(conv, f32, fast_narrow)
 
 // Max threads the (ms,ns,ks) instantiation was compiled for.
 inline int simt_thread_cap(int ms, int ns, int ks) {

@@ -551,6 +551,9 @@ void gemm(const GemmInput& in, const GemmTuning& t, const void* a, const void* b
         if (configured[pl.kind][ki] < pl.smem) {
             dev::check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)),
                        "cudaFuncSetAttribute(umma smem)");
+            dev::check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                            cudaSharedmemCarveoutMaxShared),
+                       "cudaFuncSetAttribute(carveout)");
             configured[pl.kind][ki] = pl.smem;
         }
     }

@@ -519,6 +519,9 @@ void conv(const ConvInput& in, const ConvTuning& t, const void* images, const vo
         if (configured[ki] < pl.smem) {
             dev::check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)),
                        "cudaFuncSetAttribute(umma conv smem)");
+            dev::check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                            cudaSharedmemCarveoutMaxShared),
+                       "cudaFuncSetAttribute(carveout)");
             configured[ki] = pl.smem;
         }
     }
