@@ -198,8 +198,8 @@ def cpu_baseline_sample(tuple_):
 # ---------------------------------------------------------------------------
 
 def timed_ms(launch, reps, stream, flush=True):
-    """Mean device time of `launch` (CUDA events on `stream`, L2 flushed
-    before each repetition, outside the event window)."""
+    """Mean device time of ONE cold launch (CUDA events on `stream`, L2
+    flushed before each repetition, outside the event window)."""
     import torch
 
     import paper_1802_05371_b200 as K
@@ -217,6 +217,106 @@ def timed_ms(launch, reps, stream, flush=True):
             evs.append((s0, s1))
     torch.cuda.synchronize()
     return sum(a.elapsed_time(b) for a, b in evs) / len(evs)
+
+
+def rotation(set_bytes, dev):
+    """Operand sets to rotate through so that consecutive launches never find
+    their inputs in L2: total footprint >= 2x L2 (>= 2 sets)."""
+    import torch
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    return max(2, -(-2 * l2 // max(1, set_bytes)) + 1)
+
+
+class GraphTimer:
+    """Back-to-back launches over rotating operand sets, captured once as a
+    CUDA graph of one pass over the sets (launch-bound inner loop: the host
+    never paces the GPU) and replayed; CUDA events on the launching stream
+    bracket exactly `steps` launches."""
+
+    def __init__(self, launch, n_sets, stream, warmup=3):
+        import torch
+        self.stream, self.n_sets, self.launch = stream, n_sets, launch
+        with torch.cuda.stream(stream):
+            for i in range(max(warmup, n_sets)):
+                launch(i % n_sets)
+        torch.cuda.synchronize()
+        self.graphs = {}
+
+    def _graph(self, count):
+        import torch
+        if count not in self.graphs:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.stream):
+                for i in range(count):
+                    self.launch(i % self.n_sets)
+            self.graphs[count] = g
+        return self.graphs[count]
+
+    def run_ms(self, steps, on_start=None, on_stop=None):
+        """Total device ms of `steps` launches."""
+        import torch
+        full, rem = divmod(steps, self.n_sets)
+        g_full = self._graph(self.n_sets) if full else None
+        g_rem = self._graph(rem) if rem else None
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if on_start:
+            on_start()
+        with torch.cuda.stream(self.stream):
+            s0.record(self.stream)
+            for _ in range(full):
+                g_full.replay()
+            if g_rem is not None:
+                g_rem.replay()
+            s1.record(self.stream)
+        torch.cuda.synchronize()
+        if on_stop:
+            on_stop()
+        return s0.elapsed_time(s1)
+
+    def per_launch_ms(self, steps=200):
+        return self.run_ms(steps) / steps
+
+
+def gemm_sets(inp, n_sets, dev, seed=11):
+    import torch
+    tdt = {"f32": torch.float32, "f64": torch.float64, "bf16": torch.bfloat16, "f16": torch.float16,
+           "tf32": torch.float32}[inp.dtype]
+    odt = torch.float64 if inp.dtype == "f64" else torch.float32
+    g = torch.Generator(device=dev).manual_seed(seed)
+    return [(torch.rand(inp.m * inp.k, device=dev, generator=g).to(tdt),
+             torch.rand(inp.k * inp.n, device=dev, generator=g).to(tdt),
+             torch.empty(inp.m * inp.n, device=dev, dtype=odt)) for _ in range(n_sets)]
+
+
+def gemm_set_bytes(inp):
+    es = {"f32": 4, "f64": 8, "bf16": 2, "f16": 2, "tf32": 4}[inp.dtype]
+    return (inp.m * inp.k + inp.k * inp.n) * es + inp.m * inp.n * (8 if inp.dtype == "f64" else 4)
+
+
+def time_gemm(inp, tuning, sets, stream, steps=200, mode="fast"):
+    import paper_1802_05371_b200 as K
+    sp = stream.cuda_stream
+    gt = GraphTimer(lambda i: K.execute_gemm(inp, tuning, *sets[i], mode=mode, stream=sp), len(sets), stream)
+    return gt.per_launch_ms(steps)
+
+
+def time_torch(fn_for_set, n_sets, stream, steps=200):
+    gt = GraphTimer(fn_for_set, n_sets, stream)
+    return gt.per_launch_ms(steps)
+
+
+def rerank(inp, cands, sets, stream, steps=100, mode="fast"):
+    """Re-time the screened top candidates under the reported protocol."""
+    best = None
+    for t in cands:
+        try:
+            ms = time_gemm(inp, t, sets, stream, steps, mode)
+        except Exception:  # noqa: BLE001 -- unlaunchable here: skip
+            continue
+        if best is None or ms < best[1]:
+            best = (t, ms)
+    return best
 
 
 def tuning_loop(args, ws, rank, dev):
@@ -279,85 +379,156 @@ def tuning_loop(args, ws, rank, dev):
 
 
 def other_configs(stream, dev):
-    """The other BASELINE configs on this GPU (rank 0): tensor-core skinny
-    and square GEMMs, the ResNet-style convolution, C1's fixed tuple."""
+    """The other BASELINE configs on this GPU (rank 0), each timed like the
+    headline (back-to-back launches over rotating operand sets > 2x L2, CUDA
+    graph replay, events on the launching stream) with cuBLAS / cuDNN under
+    the same protocol as context."""
     import torch
 
     import paper_1802_05371_b200 as K
-    from paper_1802_05371_b200.tuner import select_conv, select_gemm
+    from paper_1802_05371_b200.tuner import select_conv, select_gemm, tc_conv_key, tc_conv_launchable, tc_gemm_key
     pk = peaks()
     hw = K.HardwareDescriptor.b200()
-    sp = stream.cuda_stream
     res = {}
-    g = torch.Generator(device=dev).manual_seed(11)
-
-    def rnd(n, dt):
-        return torch.rand(n, device=dev, generator=g).to(dt)
-
-    # C2 bf16: skinny DeepBench on the tensor-core family (tuned over gemm_b200_tc.json)
-    inp = K.GemmInput(2560, 16, 2560, "bf16")
-    a, b = rnd(inp.m * inp.k, torch.bfloat16), rnd(inp.k * inp.n, torch.bfloat16)
-    c = torch.empty(inp.m * inp.n, device=dev)
     tc_bounds = open(os.path.join(K.FIXTURES, "bounds", "gemm_b200_tc.json")).read()
-    sel = select_gemm(inp, hw, tc_bounds, candidates=200, top_k=8)
-    ms = timed_ms(lambda: K.execute_gemm(inp, sel.tuning, a, b, c, mode="fast", stream=sp), 200, stream)
-    A2, B2 = a.view(inp.m, inp.k), b.view(inp.k, inp.n)
-    cub = timed_ms(lambda: torch.matmul(A2, B2), 200, stream)
-    byt = (inp.m * inp.k + inp.k * inp.n) * 2 + inp.m * inp.n * 4
-    res["deepbench_fprop16_bf16"] = {
-        "tflops": inp.flops / ms / 1e9, "ms": ms, "pick": sel.tuning.values(), "family": "tcgen05",
-        "roofline": {"bound": "hbm", "achieved_gbs": byt / ms / 1e6, "frac": byt / ms / 1e6 / pk["hbm_gbs"]},
-        "cublas_bf16_tflops": inp.flops / cub / 1e9, "ratio_vs_cublas": cub / ms, "l2": "flushed"}
-    # C4: 8192^3 bf16 (NN) and tf32 (NT) on tcgen05 (operands 2x128 MB / 2x256 MB > L2)
+    simt_bounds = open(os.path.join(K.FIXTURES, "bounds", "gemm_b200.json")).read()
+    torch.backends.cuda.matmul.allow_tf32 = False
+
+    def gemm_case(name, inp, bounds, key, family, candidates, cublas_tf32=False):
+        sel = select_gemm(inp, hw, bounds, candidates=candidates, top_k=8, key=key)
+        sets = gemm_sets(inp, rotation(gemm_set_bytes(inp), dev), dev)
+        t, ms = rerank(inp, [t for t, _ in sel.top], sets, stream)
+        es = {"f32": 4, "bf16": 2, "tf32": 4}[inp.dtype]
+        byt = (inp.m * inp.k + inp.k * inp.n) * es + inp.m * inp.n * 4
+        A = [x[0].view(inp.k, inp.m).t() if inp.trans_a else x[0].view(inp.m, inp.k) for x in sets]
+        B = [x[1].view(inp.n, inp.k).t() if inp.trans_b else x[1].view(inp.k, inp.n) for x in sets]
+        torch.backends.cuda.matmul.allow_tf32 = cublas_tf32
+        cub = time_torch(lambda i: torch.matmul(A[i], B[i]), len(sets), stream)
+        torch.backends.cuda.matmul.allow_tf32 = False
+        tf = inp.flops / ms / 1e9
+        ai = inp.flops / byt
+        peak_tf = pk["bf16_tflops"] if inp.dtype == "bf16" else (pk["bf16_tflops"] / 2 if inp.dtype == "tf32" else 74.4)
+        bound = "hbm" if ai * pk["hbm_gbs"] / 1e3 < peak_tf else ("tensor" if inp.dtype != "f32" else "ffma")
+        roof = ({"bound": "hbm", "achieved_gbs": byt / ms / 1e6, "peak_gbs": pk["hbm_gbs"],
+                 "frac": byt / ms / 1e6 / pk["hbm_gbs"]} if bound == "hbm" else
+                {"bound": bound, "achieved_tflops": tf, "peak_tflops": peak_tf, "frac": tf / peak_tf})
+        res[name] = {"shape": [inp.m, inp.n, inp.k], "dtype": inp.dtype, "layout": ("T" if inp.trans_a else "N") +
+                     ("T" if inp.trans_b else "N"), "tflops": tf, "us": ms * 1e3, "pick": t.values(),
+                     "family": family, "screened": sel.screened, "roofline": roof,
+                     "cublas_tflops": inp.flops / cub / 1e9, "ratio_vs_cublas": cub / ms,
+                     "rotating_sets": len(sets)}
+        del sets
+        torch.cuda.empty_cache()
+
+    # C2: skinny DeepBench / ICA on both families
+    gemm_case("deepbench_fprop16_bf16", K.GemmInput(2560, 16, 2560, "bf16"), tc_bounds, tc_gemm_key, "tcgen05", 400)
+    gemm_case("ica32_f32", K.GemmInput(32, 32, 60000, "f32", False, True), simt_bounds, None, "simt fp32", 1500)
+    gemm_case("ica32_bf16", K.GemmInput(32, 32, 60000, "bf16", False, True), tc_bounds, tc_gemm_key, "tcgen05", 400)
+    # C4: 8192^3 bf16 (NN) and tf32 (NT) on tcgen05 (operands > L2: two sets);
+    # the pick is re-timed over the 128x256 / 128x128 tiles of the tc space
     n = 8192
-    for dt, tdt, ta, tb, tup, peak in (("bf16", torch.bfloat16, False, False, (8, 8, 128, 256, 64, 1, 1, 1),
-                                        pk["bf16_tflops"]),
-                                       ("tf32", torch.float32, False, True, (8, 8, 128, 256, 32, 1, 1, 1),
-                                        pk["bf16_tflops"] / 2)):
+    for dt, ta, tb, peak in (("bf16", False, False, pk["bf16_tflops"]), ("tf32", False, True, pk["bf16_tflops"] / 2)):
         inp = K.GemmInput(n, n, n, dt, ta, tb)
-        a, b = rnd(n * n, tdt), rnd(n * n, tdt)
-        c = torch.empty(n * n, device=dev)
-        t = K.GemmTuning(*tup)
-        ms = timed_ms(lambda: K.execute_gemm(inp, t, a, b, c, mode="fast", stream=sp), 10, stream, flush=False)
+        sets = gemm_sets(inp, 2, dev)
+        es = 2 if dt == "bf16" else 4
+        cands = [K.GemmTuning(8, ns, 128, nl, u, ks, 1, 1) for nl in (256, 128) for u in (64, 128) if u * es <= 256
+                 for ks in (1, 2) for ns in (4, 16)]
+        best = None
+        for t in cands:
+            try:
+                ms = time_gemm(inp, t, sets, stream, steps=6)
+            except Exception:  # noqa: BLE001 -- does not fit this build's envelope
+                continue
+            if best is None or ms < best[1]:
+                best = (t, ms)
+        t = best[0]
+        ms = time_gemm(inp, t, sets, stream, steps=20)
+        A = [x[0].view(n, n) for x in sets]
+        B = [x[1].view(n, n).t() if tb else x[1].view(n, n) for x in sets]
         torch.backends.cuda.matmul.allow_tf32 = True
-        A2, B2 = a.view(n, n), (b.view(n, n).t() if tb else b.view(n, n))
-        cub = timed_ms(lambda: torch.matmul(A2, B2), 10, stream, flush=False)
+        cub = time_torch(lambda i: torch.matmul(A[i], B[i]), 2, stream, steps=20)
+        torch.backends.cuda.matmul.allow_tf32 = False
         tf = inp.flops / ms / 1e9
         res[f"square8192_{dt}"] = {
-            "tflops": tf, "ms": ms, "pick": list(tup), "family": "tcgen05", "layout": ("T" if ta else "N") + (
-                "T" if tb else "N"),
+            "tflops": tf, "ms": ms, "pick": t.values(), "family": "tcgen05", "layout": ("T" if ta else "N") + (
+                "T" if tb else "N"), "candidates": len(cands),
             "roofline": {"bound": "tensor", "peak_tflops": peak, "frac": tf / peak,
                          "peak_source": pk["source"] + (" cuBLAS bf16 burst" if dt == "bf16" else
                                                         " bf16 burst / 2 (tf32 rate)")},
             "cublas_tflops": inp.flops / cub / 1e9, "ratio_vs_cublas": cub / ms}
-        del a, b, c
+        del sets, A, B
         torch.cuda.empty_cache()
-    # C3 (fp32 SIMT, valid mode on a pre-padded 58x58 image = 3x3 pad 1 on 56x56)
-    cin = K.ConvInput(16, 56, 56, 64, 64, 3, 3, "f32")
-    ni, nf, no = cin.sizes()
-    img, flt = rnd(ni, torch.float32), rnd(nf, torch.float32)
-    out = torch.empty(no, device=dev)
-    cb = open(os.path.join(K.FIXTURES, "bounds", "conv_b200.json")).read()
-    csel = select_conv(cin, hw, cb, candidates=600, top_k=8)
-    ms = timed_ms(lambda: K.execute_conv(cin, csel.tuning, img, flt, out, mode="fast", stream=sp), 100, stream)
-    x = img.view(cin.c, cin.h(), cin.w(), cin.n_batch).permute(3, 0, 1, 2).contiguous()
-    w = flt.view(cin.c, cin.r, cin.s, cin.k_filters).permute(3, 0, 1, 2).contiguous()
+
+    # C3: implicit-GEMM CONV -- bf16 on tcgen05 (ResNet 56x56 + DeepBench set), fp32 SIMT ResNet
+    conv_tc_bounds = open(os.path.join(K.FIXTURES, "bounds", "conv_b200_tc.json")).read()
+    conv_simt_bounds = open(os.path.join(K.FIXTURES, "bounds", "conv_b200.json")).read()
+    torch.backends.cudnn.benchmark = True
     torch.backends.cudnn.allow_tf32 = False
-    cud = timed_ms(lambda: torch.nn.functional.conv2d(x, w), 100, stream)
-    res["conv_resnet56_f32"] = {"tflops": cin.flops / ms / 1e9, "ms": ms, "pick": csel.tuning.values(),
-                                "family": "simt fp32", "layout": "CHWN/CRSK/KPQN (reference layouts)",
-                                "cudnn_fp32_tflops_nchw": cin.flops / cud / 1e9, "ratio_vs_cudnn": cud / ms,
-                                "roofline": {"bound": "ffma", "peak_tflops": 74.4,
-                                             "frac": cin.flops / ms / 1e9 / 74.4}}
+
+    def conv_case(name, cin, bounds, key, family, candidates):
+        ni, nf, no = cin.sizes()
+        es = 2 if cin.dtype == "bf16" else 4
+        tdt = torch.bfloat16 if cin.dtype == "bf16" else torch.float32
+        sel = select_conv(cin, hw, bounds, candidates=candidates, top_k=6, key=key,
+                          accept=tc_conv_launchable(cin) if key is not None else None)
+        g = torch.Generator(device=dev).manual_seed(5)
+        n_sets = rotation((ni + nf) * es + no * 4, dev)
+        sets = [(torch.rand(ni, device=dev, generator=g).to(tdt), torch.rand(nf, device=dev, generator=g).to(tdt),
+                 torch.empty(no, device=dev)) for _ in range(n_sets)]
+        sp = stream.cuda_stream
+        best = None
+        for t, _ in sel.top:
+            try:
+                gt = GraphTimer(lambda i: K.execute_conv(cin, t, *sets[i], mode="fast", stream=sp), n_sets, stream)
+                ms = gt.per_launch_ms(100)
+            except Exception:  # noqa: BLE001
+                continue
+            if best is None or ms < best[1]:
+                best = (t, ms)
+        t, ms = best
+        # cuDNN context: the same convolution in its native NCHW layout, algorithm of its choice
+        xs = [x[0].view(cin.c, cin.h(), cin.w(), cin.n_batch).permute(3, 0, 1, 2).contiguous() for x in sets]
+        w = sets[0][1].view(cin.c, cin.r, cin.s, cin.k_filters).permute(3, 0, 1, 2).contiguous()
+        cud = time_torch(lambda i: torch.nn.functional.conv2d(xs[i], w), n_sets, stream)
+        tf = cin.flops / ms / 1e9
+        byt = (ni + nf) * es + no * 4
+        peak_tf = pk["bf16_tflops"] if cin.dtype == "bf16" else 74.4
+        ai = cin.flops / byt
+        roof = ({"bound": "hbm", "achieved_gbs": byt / ms / 1e6, "peak_gbs": pk["hbm_gbs"],
+                 "frac": byt / ms / 1e6 / pk["hbm_gbs"]} if ai * pk["hbm_gbs"] / 1e3 < peak_tf else
+                {"bound": "tensor" if cin.dtype == "bf16" else "ffma", "achieved_tflops": tf, "peak_tflops": peak_tf,
+                 "frac": tf / peak_tf})
+        res[name] = {"shape": [cin.n_batch, cin.p, cin.q, cin.k_filters, cin.c, cin.r, cin.s], "dtype": cin.dtype,
+                     "tflops": tf, "us": ms * 1e3, "pick": t.values(), "family": family, "roofline": roof,
+                     "layout": "CHWN/CRSK/KPQN (reference layouts, valid mode)",
+                     "cudnn_tflops_nchw": cin.flops / cud / 1e9, "ratio_vs_cudnn": cud / ms, "rotating_sets": n_sets}
+        del sets, xs
+        torch.cuda.empty_cache()
+
+    conv_case("conv_resnet56_bf16", K.ConvInput(16, 56, 56, 64, 64, 3, 3, "bf16"), conv_tc_bounds, tc_conv_key,
+              "tcgen05", 300)
+    for nm, cin in (("conv_ocr3_bf16", K.ConvInput(16, 24, 240, 32, 16, 3, 3, "bf16")),
+                    ("conv_face7_bf16", K.ConvInput(16, 14, 14, 48, 512, 5, 5, "bf16")),
+                    ("conv_vision10_bf16", K.ConvInput(8, 56, 56, 256, 128, 3, 3, "bf16")),
+                    ("conv_resnet13_bf16", K.ConvInput(16, 7, 7, 512, 512, 3, 3, "bf16"))):
+        try:
+            conv_case(nm, cin, conv_tc_bounds, tc_conv_key, "tcgen05", 200)
+        except Exception as e:  # noqa: BLE001 -- a shape outside the tensor-core envelope
+            res[nm] = {"error": str(e)[:200]}
+    conv_case("conv_resnet56_f32", K.ConvInput(16, 56, 56, 64, 64, 3, 3, "f32"), conv_simt_bounds, None,
+              "simt fp32", 600)
     # C1: SGEMM NN 512^3 with the paper's LINPACK(512) tuple, fast and parity modes
     inp = K.GemmInput(512, 512, 512, "f32")
-    a, b = rnd(512 * 512, torch.float32), rnd(512 * 512, torch.float32)
-    c = torch.empty(512 * 512, device=dev)
+    sets = gemm_sets(inp, rotation(gemm_set_bytes(inp), dev), dev)
     t = K.GemmTuning(2, 8, 32, 32, 8, 1, 1, 1)
     for mode in ("fast", "parity"):
-        ms = timed_ms(lambda: K.execute_gemm(inp, t, a, b, c, mode=mode, stream=sp), 200, stream)
-        res[f"sgemm512_fixed_{mode}"] = {"tflops": inp.flops / ms / 1e9, "ms": ms, "pick": t.values(),
+        ms = time_gemm(inp, t, sets, stream, 200, mode)
+        res[f"sgemm512_fixed_{mode}"] = {"tflops": inp.flops / ms / 1e9, "us": ms * 1e3, "pick": t.values(),
                                          "family": "simt fp32", "bit_exact_vs_reference": mode == "parity"}
+    A = [x[0].view(512, 512) for x in sets]
+    B = [x[1].view(512, 512) for x in sets]
+    cub = time_torch(lambda i: torch.matmul(A[i], B[i]), len(sets), stream)
+    res["sgemm512_fixed_fast"]["cublas_tflops"] = inp.flops / cub / 1e9
     return res
 
 
@@ -379,7 +550,12 @@ def our_arm(args):
     hw = K.HardwareDescriptor.b200()
     bounds = open(os.path.join(K.FIXTURES, "bounds", "gemm_b200.json")).read()
 
-    # input-aware pick (rank 0 tunes; every replica runs the same tuple)
+    stream = torch.cuda.Stream(device=dev)
+    sets = gemm_sets(inp, rotation(gemm_set_bytes(inp), dev), dev, seed=1234 + rank)
+
+    # input-aware pick (rank 0 tunes; every replica runs the same tuple):
+    # screen the legal space by single cold launches (measure), then re-rank
+    # the top candidates under the reported back-to-back protocol
     t_sel = time.perf_counter()
     if args.pick:
         pick = [int(x) for x in args.pick.split(",")]
@@ -387,8 +563,10 @@ def our_arm(args):
     elif rank == 0:
         sel = select_gemm(inp, hw, bounds, candidates=args.candidates, top_k=16, seed=0,
                           extra=[K.GemmTuning(*PAPER_TUPLE)])
-        pick = sel.tuning.values()
-        sel_info = {"screened": sel.screened, "legal_space": sel.legal_space_size, "seconds": None}
+        best_t, _ = rerank(inp, [t for t, _ in sel.top], sets, stream)
+        pick = best_t.values()
+        sel_info = {"screened": sel.screened, "legal_space": sel.legal_space_size, "seconds": None,
+                    "rerank": f"top {len(sel.top)} re-timed back-to-back"}
     else:
         pick, sel_info = None, None
     if ws > 1 and not args.pick:
@@ -397,44 +575,20 @@ def our_arm(args):
         pick, sel_info = obj
     sel_info["seconds"] = time.perf_counter() - t_sel
     tuning = K.GemmTuning(*pick)
-
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    a = torch.rand(inp.m * inp.k, device=dev, generator=gen)
-    b = torch.rand(inp.k * inp.n, device=dev, generator=gen)
-    c = torch.empty(inp.m * inp.n, device=dev)
-    stream = torch.cuda.Stream(device=dev)
     sp = stream.cuda_stream
+    timer = GraphTimer(lambda i: K.execute_gemm(inp, tuning, *sets[i], mode="fast", stream=sp), len(sets), stream,
+                       warmup=max(3, args.warmup))
+    timer.run_ms(max(3, args.warmup))  # warm-up steps through the same graph path
 
-    def step():
-        K.execute_gemm(inp, tuning, a, b, c, mode="fast", stream=sp)
-
-    with torch.cuda.stream(stream):
-        for _ in range(max(3, args.warmup)):
-            K.l2_flush(sp)
-            step()
-    torch.cuda.synchronize(dev)
-
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     clocks = ClockSampler(local)
     clocks.start()
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    clocks.active(True)
-    with torch.cuda.stream(stream):
-        for i in range(args.steps):
-            K.l2_flush(sp)
-            starts[i].record(stream)
-            step()
-            ends[i].record(stream)
-    torch.cuda.synchronize(dev)
-    clocks.active(False)
+    total_ms = timer.run_ms(args.steps, on_start=lambda: clocks.active(True), on_stop=lambda: clocks.active(False))
     if ws > 1:
         dist.barrier()
     clocks.stop()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = float(sum(step_ms))
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -448,10 +602,16 @@ def our_arm(args):
         sys.path.insert(0, os.path.join(ROOT, "tests"))
         import oracle_libs as O
         rows = 64
+        a, b, c = sets[0]
+        K.execute_gemm(inp, tuning, a, b, c, mode="fast", stream=sp)
+        torch.cuda.synchronize(dev)
         an = a.view(inp.m, inp.k)[:rows].contiguous().cpu().numpy().ravel()
         bn = b.cpu().numpy()
         ref = O.naive_gemm(rows, inp.n, inp.k, 0, 0, an, bn)
         res["max_rel_err_vs_naive_first64rows"] = O.max_rel_error(c.view(inp.m, inp.n)[:rows].cpu().numpy().ravel(), ref)
+        # one cold launch (L2 flushed before it, single launch between events) for context
+        res["cold_single_launch_us"] = timed_ms(
+            lambda: K.execute_gemm(inp, tuning, a, b, c, mode="fast", stream=sp), 100, stream) * 1e3
 
     # e2e through the public host-buffer C-ABI (H2D A,B + kernel + D2H C each step)
     e2e = None
@@ -490,23 +650,14 @@ def our_arm(args):
             dist.destroy_process_group()
         return 0
 
-    # context: cuBLAS SGEMM (TF32 off) on the same shape and flush protocol
+    # context: cuBLAS SGEMM (TF32 off) on the same shape, sets and protocol
     torch.backends.cuda.matmul.allow_tf32 = False
-    A2, B2 = a.view(inp.m, inp.k), b.view(inp.k, inp.n)
-    cub_ms = []
-    with torch.cuda.stream(stream):
-        for i in range(max(3, args.warmup)):
-            torch.matmul(A2, B2)
-        for i in range(min(args.steps, 200)):
-            K.l2_flush(sp)
-            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s0.record(stream)
-            torch.matmul(A2, B2)
-            s1.record(stream)
-            cub_ms.append((s0, s1))
-    torch.cuda.synchronize(dev)
-    cub = sum(s0.elapsed_time(s1) for s0, s1 in cub_ms) / len(cub_ms)
+    A2 = [x[0].view(inp.m, inp.k) for x in sets]
+    B2 = [x[1].view(inp.k, inp.n) for x in sets]
+    cub = time_torch(lambda i: torch.matmul(A2[i], B2[i]), len(sets), stream)
     cublas_tflops = flops / (cub * 1e-3) / 1e12
+    with torch.cuda.stream(stream):
+        cub_cold = timed_ms(lambda: torch.matmul(A2[0], B2[0]), 100, stream)
 
     pk = peaks()
     avg_ms = total_ms / args.steps
@@ -525,17 +676,21 @@ def our_arm(args):
         "data": "synthetic (torch.rand uniform [0,1) operands, resident in HBM)",
         "config": {"workload": "SGEMM 2560x16x2560 NN fp32 (DeepBench fprop N=16, BASELINE configs[1])",
                    "tuned_pick": pick, "selection": sel_info, "mode": "fast (FFMA SIMT family)",
-                   "l2": "flushed before every step (2x L2 write sweep, outside the event window)",
+                   "l2": f"inputs larger than L2: {len(sets)} rotating operand sets "
+                         f"({len(sets) * gemm_set_bytes(inp) / 2**20:.0f} MiB > 2x L2), one set per step",
+                   "timing": "CUDA events on the launching stream around exactly `steps` back-to-back launches "
+                             "(CUDA-graph replay of one pass over the sets)",
                    "parallelism": f"replicas x{ws}"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                      "algorithmic_bytes_per_launch": alg_bytes, "peak_source": pk["source"] + " burst copy"},
         "context": {"cublas_sgemm_tflops": cublas_tflops, "ratio_vs_cublas": value / ws / cublas_tflops,
-                    "ffma_fp32_peak_tflops": 74.4},
+                    "cold_single_launch_us": res.get("cold_single_launch_us"), "cublas_cold_single_launch_us":
+                    cub_cold * 1e3, "ffma_fp32_peak_tflops": 74.4},
         "cpu_baseline": cpu_baseline_sample(PAPER_TUPLE if os.environ.get("KTUNE_CPU_TUPLE") != "pick" else pick),
         "e2e": e2e,
-        "gpu_launches": 2 * args.steps,
-        "gpu_launches_detail": {"gemm": args.steps, "l2_flush": args.steps},
+        "gpu_launches": args.steps,
+        "gpu_launches_detail": {"gemm": args.steps},
         "clocks": clocks.summary(),
         "correctness": res,
         "tuning": tuning,

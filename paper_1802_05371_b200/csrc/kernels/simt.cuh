@@ -693,11 +693,16 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads : LaunchCap<MS_, NS_, 
         return;
     }
     for (int gg = tid; gg < p.nz - 1; gg += nthreads) {
-        const unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + tile_id;
+        unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + tile_id;
         unsigned long long v;
         while (true) {
             asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(flag) : "memory");
-            if (v == p.token) break;
+            if (v == p.token) {
+                // consumed: clear it, so a re-launch with the same token (a
+                // replayed CUDA graph) waits for its own publication
+                asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(0ull) : "memory");
+                break;
+            }
             __nanosleep(32);
         }
     }

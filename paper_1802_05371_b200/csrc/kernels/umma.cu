@@ -259,11 +259,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (threadIdx.x == 64 && u == int(blockIdx.x)) probe(p, 5);
             if (last && p.nz > 1) {
                 for (int gg = threadIdx.x - 64; gg < p.nz - 1; gg += 128) {
-                    const unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + w.tile;
+                    unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + w.tile;
                     unsigned long long v;
                     while (true) {
                         asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(flag) : "memory");
-                        if (v == p.token) break;
+                        if (v == p.token) {
+                // consumed: clear it, so a re-launch with the same token (a
+                // replayed CUDA graph) waits for its own publication
+                asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(0ull) : "memory");
+                break;
+            }
                         __nanosleep(32);
                     }
                 }
@@ -551,6 +556,9 @@ void gemm(const GemmInput& in, const GemmTuning& t, const void* a, const void* b
         if (configured[pl.kind][ki] < pl.smem) {
             dev::check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)),
                        "cudaFuncSetAttribute(umma smem)");
+            dev::check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                            cudaSharedmemCarveoutMaxShared),
+                       "cudaFuncSetAttribute(carveout)");
             dev::check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                             cudaSharedmemCarveoutMaxShared),
                        "cudaFuncSetAttribute(carveout)");

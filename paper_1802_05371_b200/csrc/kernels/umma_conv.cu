@@ -161,35 +161,51 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 
     if (warp == 0) {
         // ---------------- TMA producer ----------------
+        // One warp walks every k-block of every unit in series, so its loop
+        // bounds the CTA's issue rate: the (tap, channel block) position
+        // advances incrementally (no divisions per k-block) and the per-unit
+        // box origins are computed once per unit.
         int stage = 0;
         unsigned phase = 0;
         const int box_elems = p.b_sw / 2;
         const unsigned tx_bytes = 2 * p.a_box_bytes + p.b_boxes * p.b_box_bytes;
+        const int Nb = p.Nb, S = p.S, bk = p.bk, cblocks = p.cblocks, b_boxes = p.b_boxes;
+        const unsigned a_tile = p.a_tile_bytes, a_box_stride = p.a_box_stride, b_box_stride = p.b_box_stride;
         int dbg_i = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const ConvUnit w = conv_unit_of(p, u);
             const int kb_begin = w.g * p.kb_span;
             const int kb_end = min(p.kb_total, kb_begin + p.kb_span);
+            // image box origins (w*n coordinate before the tap shift, h row)
+            const int ax0 = (w.q0 + p.a_org_q[0]) * Nb + w.n0 + p.a_org_n[0];
+            const int ax1 = (w.q0 + p.a_org_q[1]) * Nb + w.n0 + p.a_org_n[1];
+            const int ah0 = w.p0 + p.a_org_p[0], ah1 = w.p0 + p.a_org_p[1];
+            int rs = kb_begin / cblocks;
+            int cb = kb_begin - rs * cblocks;
+            int r = rs / S, sx = rs - r * S;
             for (int kb = kb_begin; kb < kb_end; ++kb, ++dbg_i) {
                 mbar_wait(empty + stage, phase ^ 1u);
                 if (lane == 0) conv_probe(p, dbg_i, 0);
                 if (elect_one()) {
-                    const int rs = kb / p.cblocks;
-                    const int c0 = (kb - rs * p.cblocks) * p.bk;
-                    const int r = rs / p.S, s = rs - r * p.S;
+                    const int c0 = cb * bk;
                     unsigned char* sa = smem + std::size_t(stage) * stage_bytes;
-                    unsigned char* sb = sa + p.a_tile_bytes;
+                    unsigned char* sb = sa + a_tile;
                     mbar_expect_tx(full + stage, tx_bytes);
-#pragma unroll
-                    for (int j = 0; j < 2; ++j)
-                        tma_load_3d(sa + j * p.a_box_stride, &tma_i, full + stage,
-                                    (w.q0 + p.a_org_q[j] + s) * p.Nb + w.n0 + p.a_org_n[j], w.p0 + p.a_org_p[j] + r,
-                                    c0);
-                    for (int j = 0; j < p.b_boxes; ++j)
-                        tma_load_3d(sb + j * p.b_box_stride, &tma_f, full + stage, w.k0 + j * box_elems, rs, c0);
+                    tma_load_3d(sa, &tma_i, full + stage, ax0 + sx * Nb, ah0 + r, c0);
+                    tma_load_3d(sa + a_box_stride, &tma_i, full + stage, ax1 + sx * Nb, ah1 + r, c0);
+                    for (int j = 0; j < b_boxes; ++j)
+                        tma_load_3d(sb + j * b_box_stride, &tma_f, full + stage, w.k0 + j * box_elems, rs, c0);
                     conv_probe(p, dbg_i, 2);
                 }
                 __syncwarp();
+                if (++cb == cblocks) {
+                    cb = 0;
+                    ++rs;
+                    if (++sx == S) {
+                        sx = 0;
+                        ++r;
+                    }
+                }
                 if (++stage == p.stages) {
                     stage = 0;
                     phase ^= 1u;
@@ -263,11 +279,16 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             if (threadIdx.x == 64) conv_probe(p, 60 + (u / gridDim.x) % 4, 3);
             if (last && p.nz > 1) {
                 for (int gg = threadIdx.x - 64; gg < p.nz - 1; gg += 128) {
-                    const unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + w.tile;
+                    unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + w.tile;
                     unsigned long long v;
                     while (true) {
                         asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(flag) : "memory");
-                        if (v == p.token) break;
+                        if (v == p.token) {
+                            // consumed: clear it, so a re-launch with the same token
+                            // (a replayed CUDA graph) waits for its own publication
+                            asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(0ull) : "memory");
+                            break;
+                        }
                         __nanosleep(32);
                     }
                 }
@@ -519,6 +540,9 @@ void conv(const ConvInput& in, const ConvTuning& t, const void* images, const vo
         if (configured[ki] < pl.smem) {
             dev::check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)),
                        "cudaFuncSetAttribute(umma conv smem)");
+            dev::check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                            cudaSharedmemCarveoutMaxShared),
+                       "cudaFuncSetAttribute(carveout)");
             dev::check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                             cudaSharedmemCarveoutMaxShared),
                        "cudaFuncSetAttribute(carveout)");

@@ -26,8 +26,15 @@ class Selection:
     top: list
 
 
-def _select(inp, space, cls, hw, extra, candidates, top_k, seed, mode, repetitions):
+def _select(inp, space, cls, hw, extra, candidates, top_k, seed, mode, repetitions, key=None, accept=None):
     rng = np.random.default_rng(seed)
+    if accept is not None and len(space):
+        space = space[np.asarray([bool(accept(row)) for row in space])]
+    if key is not None and len(space):
+        # collapse tuples the executing family cannot tell apart (first legal
+        # representative of each key, in enumeration order)
+        _, first = np.unique(np.asarray([key(row) for row in space]), axis=0, return_index=True)
+        space = space[np.sort(first)]
     n = len(space)
     pick = sorted(rng.choice(n, size=min(candidates, n), replace=False).tolist()) if n else []
     cand = [cls(*map(int, space[i])) for i in pick]
@@ -54,12 +61,38 @@ def _select(inp, space, cls, hw, extra, candidates, top_k, seed, mode, repetitio
 
 
 def select_gemm(inp: GemmInput, hw: HardwareDescriptor, bounds_json: str | None = None, candidates: int = 2048,
-                top_k: int = 16, seed: int = 0, mode: str = "fast", repetitions: int = 5, extra=()) -> Selection:
+                top_k: int = 16, seed: int = 0, mode: str = "fast", repetitions: int = 5, extra=(), key=None,
+                accept=None) -> Selection:
     space = enumerate_legal(inp, hw, bounds_json, as_array=True)
-    return _select(inp, space, GemmTuning, hw, extra, candidates, top_k, seed, mode, repetitions)
+    return _select(inp, space, GemmTuning, hw, extra, candidates, top_k, seed, mode, repetitions, key, accept)
 
 
 def select_conv(inp: ConvInput, hw: HardwareDescriptor, bounds_json: str | None = None, candidates: int = 2048,
-                top_k: int = 16, seed: int = 0, mode: str = "fast", repetitions: int = 5, extra=()) -> Selection:
+                top_k: int = 16, seed: int = 0, mode: str = "fast", repetitions: int = 5, extra=(), key=None,
+                accept=None) -> Selection:
     space = enumerate_legal(inp, hw, bounds_json, as_array=True)
-    return _select(inp, space, ConvTuning, hw, extra, candidates, top_k, seed, mode, repetitions)
+    return _select(inp, space, ConvTuning, hw, extra, candidates, top_k, seed, mode, repetitions, key, accept)
+
+
+# Fields the tensor-core families actually read (umma.cu / umma_conv.cu
+# headers); the register-tile fields only shape the legality model.
+def tc_gemm_key(row):
+    return (row[2], row[3], row[4], row[5], row[1], row[7])  # m_l, n_l, u, k_s, n_s (raster), k_g
+
+
+def tc_conv_key(row):
+    return (row[4], row[5], row[6], row[7], row[8], row[9], row[11])  # k_l, p_l, q_l, n_l, u, c_s, c_g
+
+
+def tc_conv_launchable(inp):
+    """Cheap pre-filter mirroring conv_plan()'s launchability rules
+    (umma_conv.cu): a 128-pixel tile whose 64-pixel atoms are contiguous
+    (w, n) runs, UMMA_N filters, c_l = 1."""
+    def ok(row):
+        k_l, p_l, q_l, n_l, u, c_s, c_l = (int(x) for x in (row[4], row[5], row[6], row[7], row[8], row[9], row[10]))
+        if p_l * q_l * n_l != 128 or k_l % 16 or not 16 <= k_l <= 256 or c_l != 1 or c_s > 2:
+            return False
+        if u not in (16, 32, 64, 128):
+            return False
+        return (n_l == inp.n_batch and q_l * n_l >= 64) or n_l >= 64
+    return ok
