@@ -425,18 +425,18 @@ def other_configs(stream, dev):
     gemm_case("ica32_f32", K.GemmInput(32, 32, 60000, "f32", False, True), simt_bounds, None, "simt fp32", 1500)
     gemm_case("ica32_bf16", K.GemmInput(32, 32, 60000, "bf16", False, True), tc_bounds, tc_gemm_key, "tcgen05", 400)
     # C4: 8192^3 bf16 (NN) and tf32 (NT) on tcgen05 (operands > L2: two sets);
-    # the pick is re-timed over the 128x256 / 128x128 tiles of the tc space
+    # the pick is re-timed over the CTA-pair (m_l = 256) and single-CTA tiles
     n = 8192
     for dt, ta, tb, peak in (("bf16", False, False, pk["bf16_tflops"]), ("tf32", False, True, pk["bf16_tflops"] / 2)):
         inp = K.GemmInput(n, n, n, dt, ta, tb)
         sets = gemm_sets(inp, 2, dev)
         es = 2 if dt == "bf16" else 4
-        cands = [K.GemmTuning(8, ns, 128, nl, u, ks, 1, 1) for nl in (256, 128) for u in (64, 128) if u * es <= 256
-                 for ks in (1, 2) for ns in (4, 16)]
+        cands = [K.GemmTuning(8, ns, ml, nl, u, ks, 1, 1) for ml in (256, 128) for nl in (256, 128)
+                 for u in (32, 64, 128) if 64 <= u * es <= 256 for ks in (1, 2) for ns in (4, 8)]
         best = None
         for t in cands:
             try:
-                ms = time_gemm(inp, t, sets, stream, steps=6)
+                ms = time_gemm(inp, t, sets, stream, steps=8)
             except Exception:  # noqa: BLE001 -- does not fit this build's envelope
                 continue
             if best is None or ms < best[1]:

@@ -44,6 +44,7 @@ namespace tc {
 struct TcParams {
     int M, N, K;
     int bm, bn, bk;
+    int tile_m;                   // output rows per tile: 128, or 256 for a CTA pair
     int stages;
     int kb_total, kb_span, nz;
     int a_kmajor, b_kmajor;
@@ -92,6 +93,13 @@ struct Unit {
     int m0, n0, g, tile;
 };
 
+__device__ __forceinline__ void probe_kb(const TcParams& p, int i, int slot) {
+    if (p.dbg == nullptr || blockIdx.x > 1 || i >= 64) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.dbg[64 + (blockIdx.x * 64 + i) * 4 + slot] = (long long)t;
+}
+
 __device__ __forceinline__ Unit unit_of(const TcParams& p, int u) {
     Unit w;
     w.g = u % p.nz;
@@ -102,13 +110,21 @@ __device__ __forceinline__ Unit unit_of(const TcParams& p, int u) {
     const int local = t - group * per_group;
     const int mt = local / cols;
     const int nt = group * p.raster + local % cols;
-    w.m0 = mt * p.bm;
+    w.m0 = mt * p.tile_m;
     w.n0 = nt * p.bn;
     w.tile = mt * p.tiles_n + nt;
     return w;
 }
 
-template <int KIND, int KSTEPS>
+// PAIR: a cluster of two CTAs on one TPC computes a 256-row tile with
+// tcgen05.mma.cta_group::2 issued by the leader (rank 0).  Each CTA stages
+// its own 128 rows of A and half of the tile's B columns, so per CTA the
+// operand traffic per k-block is (128 + n_l/2) * u instead of (128 + n_l) * u
+// -- the L2 -> SM bandwidth (~42 B/clk/SM) is what caps the single-CTA tile.
+// Both CTAs' TMA bytes complete on the leader's full barrier; the leader's
+// commits arrive on both CTAs' empty / accumulator barriers (multicast), and
+// every epilogue thread of the pair arrives on the leader's acc_empty.
+template <int KIND, int KSTEPS, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                      const TcParams p) {
@@ -127,27 +143,40 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
     const int n_units = p.tiles_m * p.tiles_n * p.nz;
+    const unsigned rank = PAIR ? cluster_ctarank() : 0u;
+    const int cta = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);   // pair (or CTA) index
+    const int ncta = PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
+    const bool leader = rank == 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
-            mbar_init(full + s, 1);
+            mbar_init(full + s, 1);  // pair: the leader's arrive.expect_tx covers both CTAs' bytes
             mbar_init(empty + s, 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(acc_full + a, 1);
-            mbar_init(acc_empty + a, 128);
+            mbar_init(acc_empty + a, PAIR ? 256 : 128);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&tma_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&tma_b)) : "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
-                     "r"(p.tmem_cols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+        if constexpr (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(p.tmem_cols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(p.tmem_cols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();
+    if constexpr (PAIR) cluster_sync();  // peer barriers initialised before anyone signals them
+    else __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const unsigned tmem_base = *tmem_slot;
     if (threadIdx.x == 0) probe(p, 1);
@@ -158,29 +187,50 @@ __global__ void __launch_bounds__(kThreads, 1)
         unsigned phase = 0;
         const int a_box_elems = p.a_sw / p.esize, b_box_elems = p.b_sw / p.esize;
         const unsigned tx_bytes = p.a_boxes * p.a_box_bytes + p.b_boxes * p.b_box_bytes;
-        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int a_row = PAIR ? int(rank) * 128 : 0;                 // this CTA's rows of the tile
+        const int b_col = PAIR ? int(rank) * (p.bn / 2) : 0;          // this CTA's half of the columns
+        int dbg_i = 0;
+        for (int u = cta; u < n_units; u += ncta) {
             const Unit w = unit_of(p, u);
             const int kb_begin = w.g * p.kb_span;
             const int kb_end = min(p.kb_total, kb_begin + p.kb_span);
-            for (int kb = kb_begin; kb < kb_end; ++kb) {
+            for (int kb = kb_begin; kb < kb_end; ++kb, ++dbg_i) {
                 mbar_wait(empty + stage, phase ^ 1u);
+                if (lane == 0) probe_kb(p, dbg_i, 0);
                 if (elect_one()) {
-                    if (kb == kb_begin && u == int(blockIdx.x)) probe(p, 2);
+                    if (kb == kb_begin && u == cta) probe(p, 2);
                     unsigned char* sa = smem + std::size_t(stage) * stage_bytes;
                     unsigned char* sb = sa + p.a_tile_bytes;
-                    mbar_expect_tx(full + stage, tx_bytes);
                     const int k0 = kb * p.bk;
-                    for (int j = 0; j < p.a_boxes; ++j) {
-                        if (p.a_kmajor)
-                            tma_load_2d(sa + j * p.a_box_stride, &tma_a, full + stage, k0 + j * a_box_elems, w.m0);
-                        else
-                            tma_load_2d(sa + j * p.a_box_stride, &tma_a, full + stage, w.m0 + j * a_box_elems, k0);
-                    }
-                    for (int j = 0; j < p.b_boxes; ++j) {
-                        if (p.b_kmajor)
-                            tma_load_2d(sb + j * p.b_box_stride, &tma_b, full + stage, k0 + j * b_box_elems, w.n0);
-                        else
-                            tma_load_2d(sb + j * p.b_box_stride, &tma_b, full + stage, w.n0 + j * b_box_elems, k0);
+                    const int m0 = w.m0 + a_row, n0 = w.n0 + b_col;
+                    if constexpr (PAIR) {
+                        const unsigned bar = mapa_shared(smem_u32(full + stage), 0);  // the leader's
+                        // the follower's bytes may land before the leader's expect_tx:
+                        // the phase cannot complete until the leader (count 1) arrives
+                        if (leader) mbar_expect_tx(full + stage, 2 * tx_bytes);
+                        for (int j = 0; j < p.a_boxes; ++j) {
+                            if (p.a_kmajor) tma_load_2d_pair(sa + j * p.a_box_stride, &tma_a, bar, k0 + j * a_box_elems, m0);
+                            else tma_load_2d_pair(sa + j * p.a_box_stride, &tma_a, bar, m0 + j * a_box_elems, k0);
+                        }
+                        for (int j = 0; j < p.b_boxes; ++j) {
+                            if (p.b_kmajor) tma_load_2d_pair(sb + j * p.b_box_stride, &tma_b, bar, k0 + j * b_box_elems, n0);
+                            else tma_load_2d_pair(sb + j * p.b_box_stride, &tma_b, bar, n0 + j * b_box_elems, k0);
+                        }
+                        probe_kb(p, dbg_i, 1);
+                    } else {
+                        mbar_expect_tx(full + stage, tx_bytes);
+                        for (int j = 0; j < p.a_boxes; ++j) {
+                            if (p.a_kmajor)
+                                tma_load_2d(sa + j * p.a_box_stride, &tma_a, full + stage, k0 + j * a_box_elems, m0);
+                            else
+                                tma_load_2d(sa + j * p.a_box_stride, &tma_a, full + stage, m0 + j * a_box_elems, k0);
+                        }
+                        for (int j = 0; j < p.b_boxes; ++j) {
+                            if (p.b_kmajor)
+                                tma_load_2d(sb + j * p.b_box_stride, &tma_b, full + stage, k0 + j * b_box_elems, n0);
+                            else
+                                tma_load_2d(sb + j * p.b_box_stride, &tma_b, full + stage, n0 + j * b_box_elems, k0);
+                        }
                     }
                 }
                 __syncwarp();
@@ -195,85 +245,99 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Descriptors: constant high words and k-slice offsets come from the
         // host; per k-block only the 14-bit start address changes.  With
         // nacc = 2 the accumulator alternates between two TMEM column ranges,
-        // so the epilogue of one unit overlaps the MMAs of the next.
-        int stage = 0;
-        unsigned phase = 0;
-        int acc = 0;
-        unsigned acc_phase = 0;
-        const unsigned base = smem_u32(smem);
-        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-            const Unit w = unit_of(p, u);
-            const int kb_begin = w.g * p.kb_span;
-            const int nkb = min(p.kb_total, kb_begin + p.kb_span) - kb_begin;
-            mbar_wait(acc_empty + acc, acc_phase ^ 1u);
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const unsigned d_tmem = tmem_base + unsigned(acc * p.bn);
-            for (int i = 0; i < nkb; ++i) {
-                mbar_wait(full + stage, phase);
+        // so the epilogue of one unit overlaps the MMAs of the next.  In a
+        // pair only the leader issues (for both CTAs).
+        if (leader) {
+            int stage = 0;
+            unsigned phase = 0;
+            int acc = 0;
+            unsigned acc_phase = 0;
+            int dbg_i = 0;
+            const unsigned base = smem_u32(smem);
+            for (int u = cta; u < n_units; u += ncta) {
+                const Unit w = unit_of(p, u);
+                const int kb_begin = w.g * p.kb_span;
+                const int nkb = min(p.kb_total, kb_begin + p.kb_span) - kb_begin;
+                mbar_wait(acc_empty + acc, acc_phase ^ 1u);
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                if (elect_one()) {
-                    if (i == 0 && u == int(blockIdx.x)) probe(p, 3);
-                    const unsigned sa = base + unsigned(stage) * stage_bytes;
-                    const unsigned sb = sa + p.a_tile_bytes;
+                const unsigned d_tmem = tmem_base + unsigned(acc * p.bn);
+                for (int i = 0; i < nkb; ++i, ++dbg_i) {
+                    mbar_wait(full + stage, phase);
+                    if (lane == 0) probe_kb(p, dbg_i, 2);
+                    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                    if (elect_one()) {
+                        if (i == 0 && u == cta) probe(p, 3);
+                        const unsigned sa = base + unsigned(stage) * stage_bytes;
+                        const unsigned sb = sa + p.a_tile_bytes;
 #pragma unroll
-                    for (int kk = 0; kk < KSTEPS; ++kk) {
-                        const std::uint64_t adesc = (std::uint64_t(p.a_desc_hi) << 32) |
-                                                    (((sa + p.a_koff[kk]) >> 4) & 0x3FFFu) | p.a_desc_lbo;
-                        const std::uint64_t bdesc = (std::uint64_t(p.b_desc_hi) << 32) |
-                                                    (((sb + p.b_koff[kk]) >> 4) & 0x3FFFu) | p.b_desc_lbo;
-                        umma<KIND>(d_tmem, adesc, bdesc, p.idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                        for (int kk = 0; kk < KSTEPS; ++kk) {
+                            const std::uint64_t adesc = (std::uint64_t(p.a_desc_hi) << 32) |
+                                                        (((sa + p.a_koff[kk]) >> 4) & 0x3FFFu) | p.a_desc_lbo;
+                            const std::uint64_t bdesc = (std::uint64_t(p.b_desc_hi) << 32) |
+                                                        (((sb + p.b_koff[kk]) >> 4) & 0x3FFFu) | p.b_desc_lbo;
+                            if constexpr (PAIR) umma_pair<KIND>(d_tmem, adesc, bdesc, p.idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                            else umma<KIND>(d_tmem, adesc, bdesc, p.idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                        }
+                        // slot is free (in both CTAs) once these MMAs retire
+                        if constexpr (PAIR) umma_commit_pair(empty + stage);
+                        else umma_commit(empty + stage);
                     }
-                    umma_commit(empty + stage);  // slot is free once these MMAs retire
+                    __syncwarp();
+                    if (++stage == p.stages) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+                if (elect_one()) {
+                    if (u == cta) probe(p, 4);
+                    if constexpr (PAIR) umma_commit_pair(acc_full + acc);
+                    else umma_commit(acc_full + acc);
                 }
                 __syncwarp();
-                if (++stage == p.stages) {
-                    stage = 0;
-                    phase ^= 1u;
+                if (++acc == p.nacc) {
+                    acc = 0;
+                    acc_phase ^= 1u;
                 }
-            }
-            if (elect_one()) {
-                if (u == int(blockIdx.x)) probe(p, 4);
-                umma_commit(acc_full + acc);
-            }
-            __syncwarp();
-            if (++acc == p.nacc) {
-                acc = 0;
-                acc_phase ^= 1u;
             }
         }
     } else {
         // ---------------- epilogue (warps 2..5) ----------------
         const int quarter = warp & 3;  // TMEM lane quarter this warp may access
         const std::int64_t MN = std::int64_t(p.M) * p.N;
-        const std::int64_t tiles = std::int64_t(p.tiles_m) * p.tiles_n;
+        const std::int64_t tiles = std::int64_t(p.tiles_m) * p.tiles_n * (PAIR ? 2 : 1);
         const int chunk = p.bn >= 32 ? 32 : 16;
+        const unsigned acc_empty_leader0 = PAIR ? mapa_shared(smem_u32(acc_empty), 0) : smem_u32(acc_empty);
         int acc = 0;
         unsigned acc_phase = 0;
-        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        for (int u = cta; u < n_units; u += ncta) {
             const Unit w = unit_of(p, u);
             const bool last = (w.g == p.nz - 1);
-            const int row = w.m0 + quarter * 32 + lane;
-            const bool row_ok = row < p.M && quarter * 32 + lane < p.bm;
+            const int row = w.m0 + int(rank) * 128 + quarter * 32 + lane;
+            const bool row_ok = row < p.M && quarter * 32 + lane < (PAIR ? 128 : p.bm);
+            // split-K flags are per CTA-half of a pair tile
+            const std::int64_t ftile = PAIR ? (std::int64_t(w.tile / p.tiles_n) * 2 + rank) * p.tiles_n +
+                                                  w.tile % p.tiles_n
+                                            : std::int64_t(w.tile);
             mbar_wait(acc_full + acc, acc_phase);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            if (threadIdx.x == 64 && u == int(blockIdx.x)) probe(p, 5);
+            if (threadIdx.x == 64 && u == cta) probe(p, 5);
             if (last && p.nz > 1) {
                 for (int gg = threadIdx.x - 64; gg < p.nz - 1; gg += 128) {
-                    unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + w.tile;
+                    unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + ftile;
                     unsigned long long v;
                     while (true) {
                         asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(flag) : "memory");
                         if (v == p.token) {
-                // consumed: clear it, so a re-launch with the same token (a
-                // replayed CUDA graph) waits for its own publication
-                asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(0ull) : "memory");
-                break;
-            }
+                            // consumed: clear it, so a re-launch with the same token
+                            // (a replayed CUDA graph) waits for its own publication
+                            asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(0ull) : "memory");
+                            break;
+                        }
                         __nanosleep(32);
                     }
                 }
                 asm volatile("bar.sync 1, 128;\n" ::: "memory");
-                if (threadIdx.x == 64 && u == int(blockIdx.x)) probe(p, 6);
+                if (threadIdx.x == 64 && u == cta) probe(p, 6);
             }
             for (int c0 = 0; c0 < p.bn; c0 += chunk) {
                 float v[32];
@@ -283,8 +347,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (c0 + chunk >= p.bn) {
                     // accumulator fully read: hand it back to the MMA warp early
                     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(acc_empty + acc))
-                                 : "memory");
+                    if constexpr (PAIR) mbar_arrive_cluster(acc_empty_leader0 + unsigned(acc) * 8u);
+                    else mbar_arrive(acc_empty + acc);
                 }
                 if (!row_ok) continue;
                 const std::int64_t base = std::int64_t(row) * p.N + w.n0 + c0;
@@ -349,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __threadfence();
                 asm volatile("bar.sync 1, 128;\n" ::: "memory");
                 if (threadIdx.x == 64) {
-                    unsigned long long* flag = p.flags + std::int64_t(w.g) * tiles + w.tile;
+                    unsigned long long* flag = p.flags + std::int64_t(w.g) * tiles + ftile;
                     asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(p.token) : "memory");
                 }
             }
@@ -360,11 +424,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();
+    if constexpr (PAIR) cluster_sync();  // the peer's MMAs / smem reads are done before either CTA frees
+    else __syncthreads();
     if (threadIdx.x == 0) probe(p, 7);
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(p.tmem_cols));
+        if constexpr (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(p.tmem_cols));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(p.tmem_cols));
     }
 }
 
@@ -387,6 +455,7 @@ struct TcPlan {
     std::size_t ws_bytes{0}, flag_bytes{0};
     int kind{0};
     int ksteps{4};
+    bool pair{false};  // m_l = 256: cluster of two CTAs, tcgen05.mma.cta_group::2
 };
 
 
@@ -400,9 +469,13 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     TcPlan pl;
     auto& p = pl.p;
     pl.kind = in.dtype == Dtype::tf32 ? 1 : 0;
-    if (t.m_l != 128)
-        throw unsupported_error("tensor-core family: m_l must be 128 (UMMA_M) in this build, got " +
+    if (t.m_l != 128 && t.m_l != 256)
+        throw unsupported_error("tensor-core family: m_l must be 128 (one CTA) or 256 (CTA pair), got " +
                                 std::to_string(t.m_l));
+    pl.pair = t.m_l == 256;
+    if (pl.pair && (t.n_l < 32 || t.n_l % 32 != 0))
+        throw unsupported_error("tensor-core family: a CTA pair splits n_l in halves of >= 16 columns; n_l must be a "
+                                "multiple of 32, got " + std::to_string(t.n_l));
     if (t.n_l < 16 || t.n_l > 256)
         throw unsupported_error("tensor-core family: n_l must lie in [16, 256] (UMMA_N), got " + std::to_string(t.n_l));
     if (t.k_l != 1) throw unsupported_error("tensor-core family: k_l must be 1 in this build");
@@ -413,8 +486,10 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     p.M = int(in.m);
     p.N = int(in.n);
     p.K = int(in.k);
-    p.bm = t.m_l;
+    p.bm = 128;  // rows staged per CTA (a pair covers 256)
+    p.tile_m = pl.pair ? 256 : 128;
     p.bn = t.n_l;
+    const int bn_cta = pl.pair ? t.n_l / 2 : t.n_l;  // B columns staged per CTA
     p.bk = t.u;
     p.esize = es;
     p.umma_k_bytes = 32;
@@ -438,11 +513,11 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     if (p.b_kmajor) {
         p.b_sw = span_for(p.bk * es);
         p.b_boxes = p.bk * es / p.b_sw;
-        p.b_box_bytes = unsigned(p.b_sw) * p.bn;
+        p.b_box_bytes = unsigned(p.b_sw) * bn_cta;
     } else {
-        p.b_sw = span_for(p.bn * es);
-        if (p.bn * es < p.b_sw) throw unsupported_error("tensor-core family: n_l too small for an MN-major B tile");
-        p.b_boxes = p.bn * es / p.b_sw;
+        p.b_sw = span_for(bn_cta * es);
+        if (bn_cta * es < p.b_sw) throw unsupported_error("tensor-core family: n_l too small for an MN-major B tile");
+        p.b_boxes = bn_cta * es / p.b_sw;
         p.b_box_bytes = unsigned(p.b_sw) * p.bk;
     }
     p.a_box_stride = p.a_box_bytes;
@@ -466,13 +541,14 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     pl.smem = extra + stage_bytes * std::size_t(stages);
     p.nacc = (t.k_s == 2 && 2 * p.bn <= 512) ? 2 : 1;
     p.tmem_cols = std::max(32, pow2_ceil(p.nacc * p.bn));
-    p.tiles_m = int(ceil_div(in.m, p.bm));
+    p.tiles_m = int(ceil_div(in.m, pl.pair ? 256 : 128));
     p.tiles_n = int(ceil_div(in.n, p.bn));
     p.raster = std::max(1, std::min(p.tiles_n, t.n_s));
     // instruction descriptor: F32 accumulate, operand formats, majors, N>>3, M>>4
     const unsigned fmt = in.dtype == Dtype::bf16 ? 1u : (in.dtype == Dtype::f16 ? 0u : 2u);
     p.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (unsigned(p.a_kmajor ? 0 : 1) << 15) |
-              (unsigned(p.b_kmajor ? 0 : 1) << 16) | (unsigned(p.bn >> 3) << 17) | (unsigned(p.bm >> 4) << 24);
+              (unsigned(p.b_kmajor ? 0 : 1) << 16) | (unsigned(p.bn >> 3) << 17) |
+              (unsigned((pl.pair ? 256 : 128) >> 4) << 24);
     // Shared-memory matrix descriptors (tcgen05 "version 1"): high word =
     // SBO (8 rows x swizzle span) | version 1 | swizzle layout; LBO = 16 B for
     // K-major (unused with swizzle), = box stride between MN atoms for
@@ -500,9 +576,15 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     // round-robin over (tile, slice) units
     const std::int64_t units = std::int64_t(p.tiles_m) * p.tiles_n * p.nz;
     if (units > 0x7fffffff) throw unsupported_error("too many work units for one launch");
-    pl.grid = dim3(unsigned(std::min<std::int64_t>(units, num_sms())), 1, 1);
+    if (pl.pair) {
+        // one CTA per SM, two per cluster: at most (SMs / 2) co-resident pairs
+        pl.grid = dim3(unsigned(2 * std::min<std::int64_t>(units, num_sms() / 2)), 1, 1);
+    } else {
+        pl.grid = dim3(unsigned(std::min<std::int64_t>(units, num_sms())), 1, 1);
+    }
     if (p.nz > 1) {
-        pl.flag_bytes = (std::size_t(p.tiles_m) * p.tiles_n * std::size_t(p.nz - 1) * 8 + 255) / 256 * 256;
+        pl.flag_bytes = (std::size_t(p.tiles_m) * (pl.pair ? 2 : 1) * p.tiles_n * std::size_t(p.nz - 1) * 8 + 255) /
+                        256 * 256;
         pl.ws_bytes = pl.flag_bytes + std::size_t(p.nz - 1) * std::size_t(in.m) * std::size_t(in.n) * 4;
     }
     return pl;
@@ -539,34 +621,53 @@ void gemm(const GemmInput& in, const GemmTuning& t, const void* a, const void* b
     // A: K-major -> [M][K] rows, boxes {a_sw/es along K, bm}; MN-major -> [K][M], boxes {a_sw/es along M, bk}
     CUtensorMap ma = p.a_kmajor ? make_map(a, in.dtype, in.k, in.m, p.a_sw / es, p.bm, p.a_sw)
                                 : make_map(a, in.dtype, in.m, in.k, p.a_sw / es, p.bk, p.a_sw);
-    CUtensorMap mb = p.b_kmajor ? make_map(b, in.dtype, in.k, in.n, p.b_sw / es, p.bn, p.b_sw)
+    CUtensorMap mb = p.b_kmajor ? make_map(b, in.dtype, in.k, in.n, p.b_sw / es, pl.pair ? p.bn / 2 : p.bn, p.b_sw)
                                 : make_map(b, in.dtype, in.n, in.k, p.b_sw / es, p.bk, p.b_sw);
     using ktune_dev::tc::umma_gemm_kernel;
-    static const void* const kernels[2][4] = {
-        {reinterpret_cast<const void*>(&umma_gemm_kernel<0, 1>), reinterpret_cast<const void*>(&umma_gemm_kernel<0, 2>),
-         reinterpret_cast<const void*>(&umma_gemm_kernel<0, 4>), reinterpret_cast<const void*>(&umma_gemm_kernel<0, 8>)},
-        {reinterpret_cast<const void*>(&umma_gemm_kernel<1, 1>), reinterpret_cast<const void*>(&umma_gemm_kernel<1, 2>),
-         reinterpret_cast<const void*>(&umma_gemm_kernel<1, 4>), reinterpret_cast<const void*>(&umma_gemm_kernel<1, 8>)}};
+#define KTUNE_TC_ROW(K, P)                                                                           \
+    {reinterpret_cast<const void*>(&umma_gemm_kernel<K, 1, P>), reinterpret_cast<const void*>(&umma_gemm_kernel<K, 2, P>), \
+     reinterpret_cast<const void*>(&umma_gemm_kernel<K, 4, P>), reinterpret_cast<const void*>(&umma_gemm_kernel<K, 8, P>)}
+    static const void* const kernels[2][2][4] = {{KTUNE_TC_ROW(0, false), KTUNE_TC_ROW(1, false)},
+                                                 {KTUNE_TC_ROW(0, true), KTUNE_TC_ROW(1, true)}};
+#undef KTUNE_TC_ROW
     const int ki = pl.ksteps == 1 ? 0 : (pl.ksteps == 2 ? 1 : (pl.ksteps == 4 ? 2 : 3));
-    const void* kern = kernels[pl.kind][ki];
+    const void* kern = kernels[pl.pair ? 1 : 0][pl.kind][ki];
     {
         static std::mutex mu;
-        static std::size_t configured[2][4] = {};
+        static std::size_t configured[2][2][4] = {};
         std::lock_guard<std::mutex> lock(mu);
-        if (configured[pl.kind][ki] < pl.smem) {
+        std::size_t& done = configured[pl.pair ? 1 : 0][pl.kind][ki];
+        if (done < pl.smem) {
             dev::check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)),
                        "cudaFuncSetAttribute(umma smem)");
             dev::check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                             cudaSharedmemCarveoutMaxShared),
                        "cudaFuncSetAttribute(carveout)");
-            dev::check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                            cudaSharedmemCarveoutMaxShared),
-                       "cudaFuncSetAttribute(carveout)");
-            configured[pl.kind][ki] = pl.smem;
+            if (pl.pair)
+                dev::check(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0),
+                           "cudaFuncSetAttribute(cluster)");
+            done = pl.smem;
         }
     }
     void* args[] = {&ma, &mb, &p};
-    dev::check(cudaLaunchKernel(kern, pl.grid, dim3(ktune_dev::tc::kThreads), args, pl.smem, stream), "umma launch");
+    if (!pl.pair) {
+        dev::check(cudaLaunchKernel(kern, pl.grid, dim3(ktune_dev::tc::kThreads), args, pl.smem, stream),
+                   "umma launch");
+        return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = pl.grid;
+    cfg.blockDim = dim3(ktune_dev::tc::kThreads);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    dev::check(cudaLaunchKernelExC(&cfg, kern, args), "umma pair launch");
 }
 
 }  // namespace umma
