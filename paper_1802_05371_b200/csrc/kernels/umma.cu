@@ -129,6 +129,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                      const TcParams p) {
     if (threadIdx.x == 0) probe(p, 0);
+    if (threadIdx.x == 0 && p.dbg != nullptr) {  // per-CTA start / end (debug timeline)
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.dbg[1024 + blockIdx.x * 4] = (long long)t;
+    }
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-align the tile region (SW128 atoms repeat every 1024 bytes).
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
@@ -321,6 +326,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(acc_full + acc, acc_phase);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             if (threadIdx.x == 64 && u == cta) probe(p, 5);
+            if (threadIdx.x == 64 && p.dbg != nullptr) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                p.dbg[1024 + blockIdx.x * 4 + 1] = (long long)t;
+            }
             if (last && p.nz > 1) {
                 for (int gg = threadIdx.x - 64; gg < p.nz - 1; gg += 128) {
                     unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + ftile;
@@ -338,6 +348,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 asm volatile("bar.sync 1, 128;\n" ::: "memory");
                 if (threadIdx.x == 64 && u == cta) probe(p, 6);
+                if (threadIdx.x == 64 && p.dbg != nullptr) {
+                    unsigned long long t;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                    p.dbg[1024 + blockIdx.x * 4 + 2] = (long long)t;
+                }
             }
             for (int c0 = 0; c0 < p.bn; c0 += chunk) {
                 float v[32];
@@ -360,29 +375,41 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (p.nz > 1) {
                         // ordered fold of the published partials; every partial of
                         // one slice is loaded before any add (one L2 round trip per slice)
+                        // FB slices per batch: all their loads are in flight
+                        // together, then the adds run in slice order
+                        constexpr int FB = 2;
                         float accv[32];
 #pragma unroll
                         for (int i = 0; i < 32; ++i) accv[i] = 0.f;
-                        for (int gg = 0; gg < p.nz - 1; ++gg) {
-                            const float* src = p.ws + gg * MN + base;
-                            float part[32];
-                            if (vec) {
+                        for (int g0 = 0; g0 < p.nz - 1; g0 += FB) {
+                            float part[FB][32];
 #pragma unroll
-                                for (int i = 0; i < 32; i += 4) {
-                                    if (i < chunk) {
-                                        const float4 q = __ldcg(reinterpret_cast<const float4*>(src + i));
-                                        part[i] = q.x;
-                                        part[i + 1] = q.y;
-                                        part[i + 2] = q.z;
-                                        part[i + 3] = q.w;
+                            for (int f = 0; f < FB; ++f) {
+                                const bool live = g0 + f < p.nz - 1;
+                                const float* src = p.ws + (g0 + f) * MN + base;
+                                if (vec) {
+#pragma unroll
+                                    for (int i = 0; i < 32; i += 4) {
+                                        if (i < chunk && live) {
+                                            const float4 q = __ldcg(reinterpret_cast<const float4*>(src + i));
+                                            part[f][i] = q.x;
+                                            part[f][i + 1] = q.y;
+                                            part[f][i + 2] = q.z;
+                                            part[f][i + 3] = q.w;
+                                        } else {
+                                            part[f][i] = part[f][i + 1] = part[f][i + 2] = part[f][i + 3] = 0.f;
+                                        }
                                     }
-                                }
-                            } else {
+                                } else {
 #pragma unroll
-                                for (int i = 0; i < 32; ++i) part[i] = i < ncols ? __ldcg(src + i) : 0.f;
+                                    for (int i = 0; i < 32; ++i) part[f][i] = (live && i < ncols) ? __ldcg(src + i) : 0.f;
+                                }
                             }
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) accv[i] = __fadd_rn(accv[i], part[i]);
+                            for (int f = 0; f < FB; ++f)
+                                if (g0 + f < p.nz - 1)
+#pragma unroll
+                                    for (int i = 0; i < 32; ++i) accv[i] = __fadd_rn(accv[i], part[f][i]);
                         }
 #pragma unroll
                         for (int i = 0; i < 32; ++i) v[i] = __fadd_rn(accv[i], v[i]);
@@ -410,11 +437,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             if (!last && p.nz > 1) {
-                __threadfence();
+                // bar.sync orders the 128 threads' partial stores before one
+                // thread's cumulative gpu-scope release (no per-thread fence)
                 asm volatile("bar.sync 1, 128;\n" ::: "memory");
                 if (threadIdx.x == 64) {
                     unsigned long long* flag = p.flags + std::int64_t(w.g) * tiles + ftile;
-                    asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(p.token) : "memory");
+                    asm volatile("fence.acq_rel.gpu;\nst.release.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(p.token)
+                                 : "memory");
                 }
             }
             if (++acc == p.nacc) {
@@ -427,6 +456,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (PAIR) cluster_sync();  // the peer's MMAs / smem reads are done before either CTA frees
     else __syncthreads();
     if (threadIdx.x == 0) probe(p, 7);
+    if (threadIdx.x == 0 && p.dbg != nullptr) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.dbg[1024 + blockIdx.x * 4 + 3] = (long long)t;
+    }
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         if constexpr (PAIR)
@@ -580,7 +614,22 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
         // one CTA per SM, two per cluster: at most (SMs / 2) co-resident pairs
         pl.grid = dim3(unsigned(2 * std::min<std::int64_t>(units, num_sms() / 2)), 1, 1);
     } else {
-        pl.grid = dim3(unsigned(std::min<std::int64_t>(units, num_sms())), 1, 1);
+        // Short units (few k-blocks, more units than SMs -- split-K skinny
+        // shapes): two co-resident CTAs per SM, each with a pipeline just deep
+        // enough for its slice, keep twice the loads in flight per SM and run
+        // every unit in one wave instead of two rounds of the persistent loop.
+        const std::size_t per_sm = std::size_t(smem_per_sm());
+        const int kb_unit = p.kb_span;
+        const std::size_t half = per_sm / 2 > 1024 + extra ? per_sm / 2 - 1024 : 0;  // 1 KB reserved per CTA
+        const int stages2 = half > extra ? int((half - extra) / stage_bytes) : 0;
+        const int tmem_ok = 2 * p.tmem_cols <= 512;
+        if (units > num_sms() && tmem_ok && stages2 >= std::min(kb_unit, 3) && stages2 >= 2) {
+            p.stages = std::min(stages2, std::max(2, kb_unit));
+            pl.smem = extra + stage_bytes * std::size_t(p.stages);
+            pl.grid = dim3(unsigned(std::min<std::int64_t>(units, 2 * num_sms())), 1, 1);
+        } else {
+            pl.grid = dim3(unsigned(std::min<std::int64_t>(units, num_sms())), 1, 1);
+        }
     }
     if (p.nz > 1) {
         pl.flag_bytes = (std::size_t(p.tiles_m) * (pl.pair ? 2 : 1) * p.tiles_n * std::size_t(p.nz - 1) * 8 + 255) /

@@ -250,6 +250,16 @@ inline int smem_optin() {
     return v;
 }
 
+inline int smem_per_sm() {
+    static int v = [] {
+        int dev = 0, x = 0;
+        dev::check(cudaGetDevice(&dev), "cudaGetDevice");
+        dev::check(cudaDeviceGetAttribute(&x, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev), "smem/SM attr");
+        return x;
+    }();
+    return v;
+}
+
 inline int pow2_ceil(int x) {
     int v = 1;
     while (v < x) v <<= 1;
