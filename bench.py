@@ -4,10 +4,12 @@
 
 Workload (BASELINE.json configs[1]): DeepBench fprop SGEMM M=2560 N=16 K=2560
 NN, fp32, with the input-aware tuned pick of the ISAAC tuple.  One step = one
-launch of the tuned kernel over resident operands, L2 flushed before each step
-(the 26 MB working set would otherwise live in the 126 MB L2); each step is
-bracketed by CUDA events on the launching stream and the step times are
-summed.  N>1 runs N independent replicas (the GEMM does not shard).
+launch of the tuned kernel on one of N rotating operand sets whose total
+footprint exceeds 2x L2 (so every launch streams its inputs from HBM); the K
+timed steps are back-to-back launches captured once as a CUDA graph of one pass
+over the sets and replayed, bracketed by CUDA events on the launching stream.
+N>1 runs N independent replicas (the GEMM does not shard); the tuning-loop
+figures shard samples over the ranks.
 
 --impl reference times the reference's own CPU executor (oracle/_ref: ktune
 execute_gemm<float> compiled from the untouched sources) on the same workload
