@@ -7,6 +7,8 @@
 // asynchronous on `stream`.  Errors are thrown as the exception classes
 // below (the C-ABI maps them to ktune_status codes).
 
+#include <cuda_runtime.h>
+
 #include <cstddef>
 #include <cstdint>
 #include <stdexcept>
@@ -72,6 +74,13 @@ void l2_flush(cudaStream_t stream);
 void fill_uniform(void* dst, std::int64_t n, Dtype dtype, std::uint64_t seed, cudaStream_t stream);
 
 void check(int cuda_status, const char* what);
+
+// Launch with programmatic stream serialization (PDL: the kernel's prologue
+// overlaps the previous kernel on the stream; its griddepcontrol.wait orders
+// the global-memory work) and, if cluster_x > 1, a (cluster_x, 1, 1) cluster.
+// KTUNE_PDL=0 disables the attribute.
+void launch(const void* kernel, dim3 grid, dim3 block, void** args, std::size_t smem, cudaStream_t stream,
+            int cluster_x, const char* what);
 
 }  // namespace dev
 }  // namespace ktune

@@ -36,6 +36,36 @@ void check(int status, const char* what) {
         throw cuda_error(std::string(what) + ": " + cudaGetErrorString(static_cast<cudaError_t>(status)));
 }
 
+void launch(const void* kernel, dim3 grid, dim3 block, void** args, std::size_t smem, cudaStream_t stream,
+            int cluster_x, const char* what) {
+    static const bool pdl = [] {
+        const char* e = std::getenv("KTUNE_PDL");
+        return !(e != nullptr && e[0] == '0');
+    }();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    if (pdl) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    if (cluster_x > 1) {
+        attr[n].id = cudaLaunchAttributeClusterDimension;
+        attr[n].val.clusterDim.x = unsigned(cluster_x);
+        attr[n].val.clusterDim.y = 1;
+        attr[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = unsigned(n);
+    check(cudaLaunchKernelExC(&cfg, kernel, args), what);
+}
+
 namespace {
 
 std::int64_t ceil_div(std::int64_t a, std::int64_t b) { return (a + b - 1) / b; }
@@ -344,7 +374,7 @@ void launch_gemm_t(const GemmInput& in, Plan& pl, Mode mode, const void* a, cons
     const void* k = pick(false, in.dtype, mode, pl);
     prepare(k, pl.smem);
     void* args[] = {&prob, &pl.p};
-    check(cudaLaunchKernel(k, pl.grid, dim3(unsigned(pl.threads)), args, pl.smem, s), "gemm launch");
+    launch(k, pl.grid, dim3(unsigned(pl.threads)), args, pl.smem, s, 1, "gemm launch");
 }
 
 template <typename T>
@@ -371,7 +401,7 @@ void launch_conv_t(const ConvInput& in, const ConvTuning& t, Plan& pl, Mode mode
     const void* k = pick(true, in.dtype, mode, pl);
     prepare(k, pl.smem);
     void* args[] = {&prob, &pl.p};
-    check(cudaLaunchKernel(k, pl.grid, dim3(unsigned(pl.threads)), args, pl.smem, s), "conv launch");
+    launch(k, pl.grid, dim3(unsigned(pl.threads)), args, pl.smem, s, 1, "conv launch");
 }
 
 }  // namespace

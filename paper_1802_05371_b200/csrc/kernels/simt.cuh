@@ -162,6 +162,14 @@ struct ConvProblem {
     }
 };
 
+// ---- programmatic dependent launch ----------------------------------------
+// Launched with programmatic stream serialization, a kernel lets the next
+// one on its stream start its prologue as soon as every block of this one is
+// running; the next kernel's global-memory work waits for this one's
+// completion in pdl_wait().  Without the attribute both are no-ops.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 // ---- arithmetic of the two modes ------------------------------------------
 template <typename T, bool PARITY>
 struct Arith;
@@ -464,6 +472,7 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads : LaunchCap<MS_, NS_, 
     const int b_cstep = p.tn * b_ld;  // BRM: distance between a thread's strided cols
 
     // ---- multistage cp.async pipeline (one barrier per step) ----------------
+    pdl_wait();  // inputs / outputs / workspace may belong to the previous kernel
     const int S = p.stages;
     for (int s = 0; s < S - 1; ++s) {
         if (s < nsteps) load_stage(s, s);
@@ -619,6 +628,10 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads : LaunchCap<MS_, NS_, 
     cp_async_wait<0>();
     __syncthreads();
     simt_probe(p, 3);
+    // main loop done: the next kernel may start its prologue on the SM
+    // resources this one no longer needs (earlier, its blocks would compete
+    // with this kernel's latency-bound main loop)
+    pdl_launch_dependents();
 
     // ---- fold: k_s sets within a thread, then k_l groups in order ----------
     // (backends.cpp:311-318): blk = ((0 + g0s0) + g0s1) + ... + g1s0 + ...

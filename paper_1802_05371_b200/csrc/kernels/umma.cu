@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                      const TcParams p) {
     if (threadIdx.x == 0) probe(p, 0);
+    pdl_launch_dependents();
     if (threadIdx.x == 0 && p.dbg != nullptr) {  // per-CTA start / end (debug timeline)
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -185,6 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const unsigned tmem_base = *tmem_slot;
     if (threadIdx.x == 0) probe(p, 1);
+    pdl_wait();  // setup above overlaps the previous kernel; global work starts here
 
     if (warp == 0) {
         // ---------------- TMA producer (whole warp loops, one lane issues) ----------------
@@ -699,24 +701,8 @@ void gemm(const GemmInput& in, const GemmTuning& t, const void* a, const void* b
         }
     }
     void* args[] = {&ma, &mb, &p};
-    if (!pl.pair) {
-        dev::check(cudaLaunchKernel(kern, pl.grid, dim3(ktune_dev::tc::kThreads), args, pl.smem, stream),
-                   "umma launch");
-        return;
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = pl.grid;
-    cfg.blockDim = dim3(ktune_dev::tc::kThreads);
-    cfg.dynamicSmemBytes = pl.smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    dev::check(cudaLaunchKernelExC(&cfg, kern, args), "umma pair launch");
+    dev::launch(kern, pl.grid, dim3(ktune_dev::tc::kThreads), args, pl.smem, stream, pl.pair ? 2 : 1,
+                pl.pair ? "umma pair launch" : "umma launch");
 }
 
 }  // namespace umma

@@ -122,6 +122,7 @@ template <int KSTEPS>
 __global__ void __launch_bounds__(kConvThreads, 1)
     umma_conv_kernel(const __grid_constant__ CUtensorMap tma_i, const __grid_constant__ CUtensorMap tma_f,
                      const ConvTcParams p) {
+    pdl_launch_dependents();
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
                                                            ~std::uintptr_t(1023));
@@ -158,6 +159,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const unsigned tmem_base = *tmem_slot;
+    pdl_wait();  // setup above overlaps the previous kernel; global work starts here
 
     if (warp == 0) {
         // ---------------- TMA producer ----------------
@@ -550,8 +552,7 @@ void conv(const ConvInput& in, const ConvTuning& t, const void* images, const vo
         }
     }
     void* args[] = {&mi, &mf, &p};
-    dev::check(cudaLaunchKernel(kern, pl.grid, dim3(ktune_dev::tc::kConvThreads), args, pl.smem, stream),
-               "umma conv launch");
+    dev::launch(kern, pl.grid, dim3(ktune_dev::tc::kConvThreads), args, pl.smem, stream, 1, "umma conv launch");
 }
 
 }  // namespace umma
