@@ -355,6 +355,8 @@ Plan conv_plan(const ConvInput& in, const ConvTuning& t, const void* img = nullp
     require_divisible(t.u, t.c_s, "u not divisible by c_s");
     if (in.dtype != Dtype::f32 && in.dtype != Dtype::f64)
         throw unsupported_error(std::string("simt family does not execute ") + to_string(in.dtype));
+    if (in.c * in.r * in.s + t.u >= (std::int64_t(1) << 31))
+        throw unsupported_error("simt conv: the reduction C*R*S must fit in 31 bits");
     const int es = dtype_size_bytes(in.dtype);
     const std::int64_t col_tiles = ceil_div(in.p, t.p_l) * ceil_div(in.q, t.q_l) * ceil_div(in.n_batch, t.n_l);
     auto va = [&](int, std::int64_t) { return vec_width(es, {in.k_filters}, {flt}, t.k_l); };

@@ -130,13 +130,17 @@ struct ConvProblem {
     // chunk is entirely valid or entirely outside the tensor.
     __device__ int b_cols_valid(std::int64_t base, int v) const { return base < 0 ? 0 : v; }
     __device__ const T* a_addr(std::int64_t row, std::int64_t t) const { return flt + t * K + row; }
+    // t = (c*R + r)*S + s -> image offset of the tap (the indirection table
+    // entry of backends.cpp:197-216).  The reduction index fits in 32 bits
+    // (host-checked), so the decomposition uses 32-bit divisions: the 64-bit
+    // ones dominated the gather loader's instruction count.
     __device__ std::int64_t off(std::int64_t t) const {
-        const std::int64_t rs = R * S;
-        const std::int64_t c = t / rs;
-        const std::int64_t rem = t - c * rs;
-        const std::int64_t r = rem / S;
-        const std::int64_t s = rem - r * S;
-        return (c * H + r) * W * Nb + s * Nb;
+        const unsigned tt = unsigned(t), rs = unsigned(R * S), ss = unsigned(S);
+        const unsigned c = tt / rs;
+        const unsigned rem = tt - c * rs;
+        const unsigned r = rem / ss;
+        const unsigned s = rem - r * ss;
+        return (std::int64_t(c) * H + r) * W * Nb + std::int64_t(s) * Nb;
     }
     __device__ const T* b_addr(std::int64_t t, std::int64_t base) const { return img + base + off(t); }
     __device__ void column(int ct, int x, std::int64_t& base, std::int64_t& out_col) const {
