@@ -43,7 +43,9 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML
+    (~1 ms per query, every 5 ms) so even a short region gets samples;
+    nvidia-smi as the fallback when NVML is unavailable."""
 
     Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -54,8 +56,27 @@ class ClockSampler:
         self._stop = threading.Event()
         self._active = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(device_index))
+        except Exception:  # noqa: BLE001 -- fall back to nvidia-smi
+            self._nvml = None
 
     def _query(self):
+        if self._nvml is not None:
+            try:
+                nv, h = self._nvml
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                return dict(sm=float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                            max=float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)),
+                            hw="Active" if r & nv.nvmlClocksEventReasonHwSlowdown else "Not Active",
+                            hw_thermal="Active" if r & nv.nvmlClocksEventReasonHwThermalSlowdown else "Not Active",
+                            sw_thermal="Active" if r & nv.nvmlClocksEventReasonSwThermalSlowdown else "Not Active",
+                            power_cap="Active" if r & nv.nvmlClocksEventReasonSwPowerCap else "Not Active")
+            except Exception:  # noqa: BLE001
+                return None
         try:
             out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
                                  capture_output=True, text=True, timeout=5).stdout.strip()
@@ -65,12 +86,13 @@ class ClockSampler:
             return None
 
     def _run(self):
+        period = 0.005 if self._nvml is not None else 0.1
         while not self._stop.is_set():
             if self._active.is_set():
                 s = self._query()
                 if s is not None and self._active.is_set():
                     self.samples.append(s)
-            self._stop.wait(0.1)
+            self._stop.wait(period)
 
     def start(self):
         self._t.start()
@@ -81,6 +103,7 @@ class ClockSampler:
     def stop(self):
         self._stop.set()
         self._t.join(timeout=10)
+        self.during = len(self.samples)
         if not self.samples:  # region shorter than one query: take one now (device still warm)
             s = self._query()
             if s:
@@ -97,7 +120,8 @@ class ClockSampler:
                 if s[key].lower() == "active":
                     reasons.add(name)
         return {"sm_mhz": sms[len(sms) // 2], "sm_max_mhz": self.samples[0]["max"], "reasons": sorted(reasons),
-                "n_samples": len(self.samples)}
+                "n_samples": len(self.samples), "samples_during_timed_region": getattr(self, "during", None),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def dist_env():
