@@ -377,42 +377,48 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (p.nz > 1) {
                         // ordered fold of the published partials; every partial of
                         // one slice is loaded before any add (one L2 round trip per slice)
-                        // FB slices per batch: all their loads are in flight
-                        // together, then the adds run in slice order
-                        constexpr int FB = 2;
+                        // Slices are folded in batches whose loads are all in
+                        // flight together (then added in slice order): 8 slices of
+                        // a 16-column chunk or 4 of a 32-column one per batch, so
+                        // a deep split (ICA: k_g = 32) costs a few L2 round trips.
                         float accv[32];
 #pragma unroll
                         for (int i = 0; i < 32; ++i) accv[i] = 0.f;
-                        for (int g0 = 0; g0 < p.nz - 1; g0 += FB) {
-                            float part[FB][32];
+                        auto fold = [&]<int CH, int FB>() {
+                            for (int g0 = 0; g0 < p.nz - 1; g0 += FB) {
+                                float part[FB][CH];
 #pragma unroll
-                            for (int f = 0; f < FB; ++f) {
-                                const bool live = g0 + f < p.nz - 1;
-                                const float* src = p.ws + (g0 + f) * MN + base;
-                                if (vec) {
+                                for (int f = 0; f < FB; ++f) {
+                                    const bool live = g0 + f < p.nz - 1;
+                                    const float* src = p.ws + (g0 + f) * MN + base;
+                                    if (vec) {
 #pragma unroll
-                                    for (int i = 0; i < 32; i += 4) {
-                                        if (i < chunk && live) {
-                                            const float4 q = __ldcg(reinterpret_cast<const float4*>(src + i));
-                                            part[f][i] = q.x;
-                                            part[f][i + 1] = q.y;
-                                            part[f][i + 2] = q.z;
-                                            part[f][i + 3] = q.w;
-                                        } else {
-                                            part[f][i] = part[f][i + 1] = part[f][i + 2] = part[f][i + 3] = 0.f;
+                                        for (int i = 0; i < CH; i += 4) {
+                                            if (live) {
+                                                const float4 q = __ldcg(reinterpret_cast<const float4*>(src + i));
+                                                part[f][i] = q.x;
+                                                part[f][i + 1] = q.y;
+                                                part[f][i + 2] = q.z;
+                                                part[f][i + 3] = q.w;
+                                            } else {
+                                                part[f][i] = part[f][i + 1] = part[f][i + 2] = part[f][i + 3] = 0.f;
+                                            }
                                         }
+                                    } else {
+#pragma unroll
+                                        for (int i = 0; i < CH; ++i)
+                                            part[f][i] = (live && i < ncols) ? __ldcg(src + i) : 0.f;
                                     }
-                                } else {
-#pragma unroll
-                                    for (int i = 0; i < 32; ++i) part[f][i] = (live && i < ncols) ? __ldcg(src + i) : 0.f;
                                 }
+#pragma unroll
+                                for (int f = 0; f < FB; ++f)
+                                    if (g0 + f < p.nz - 1)
+#pragma unroll
+                                        for (int i = 0; i < CH; ++i) accv[i] = __fadd_rn(accv[i], part[f][i]);
                             }
-#pragma unroll
-                            for (int f = 0; f < FB; ++f)
-                                if (g0 + f < p.nz - 1)
-#pragma unroll
-                                    for (int i = 0; i < 32; ++i) accv[i] = __fadd_rn(accv[i], part[f][i]);
-                        }
+                        };
+                        if (chunk == 16) fold.template operator()<16, 8>();
+                        else fold.template operator()<32, 4>();
 #pragma unroll
                         for (int i = 0; i < 32; ++i) v[i] = __fadd_rn(accv[i], v[i]);
                     }
