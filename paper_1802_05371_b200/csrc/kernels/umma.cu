@@ -622,22 +622,9 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
         // one CTA per SM, two per cluster: at most (SMs / 2) co-resident pairs
         pl.grid = dim3(unsigned(2 * std::min<std::int64_t>(units, num_sms() / 2)), 1, 1);
     } else {
-        // Short units (few k-blocks, more units than SMs -- split-K skinny
-        // shapes): two co-resident CTAs per SM, each with a pipeline just deep
-        // enough for its slice, keep twice the loads in flight per SM and run
-        // every unit in one wave instead of two rounds of the persistent loop.
-        const std::size_t per_sm = std::size_t(smem_per_sm());
-        const int kb_unit = p.kb_span;
-        const std::size_t half = per_sm / 2 > 1024 + extra ? per_sm / 2 - 1024 : 0;  // 1 KB reserved per CTA
-        const int stages2 = half > extra ? int((half - extra) / stage_bytes) : 0;
-        const int tmem_ok = 2 * p.tmem_cols <= 512;
-        if (units > num_sms() && tmem_ok && stages2 >= std::min(kb_unit, 3) && stages2 >= 2) {
-            p.stages = std::min(stages2, std::max(2, kb_unit));
-            pl.smem = extra + stage_bytes * std::size_t(p.stages);
-            pl.grid = dim3(unsigned(std::min<std::int64_t>(units, 2 * num_sms())), 1, 1);
-        } else {
-            pl.grid = dim3(unsigned(std::min<std::int64_t>(units, num_sms())), 1, 1);
-        }
+        // one CTA per SM: the epilogue's batched split-K fold needs ~240
+        // registers per thread, so two 192-thread CTAs never co-reside
+        pl.grid = dim3(unsigned(std::min<std::int64_t>(units, num_sms())), 1, 1);
     }
     if (p.nz > 1) {
         pl.flag_bytes = (std::size_t(p.tiles_m) * (pl.pair ? 2 : 1) * p.tiles_n * std::size_t(p.nz - 1) * 8 + 255) /
