@@ -134,6 +134,22 @@ def test_host_buffer_entry_point_bitwise(cuda):
         K.execute_gemm_host(inp, t, a[:-1], b)
 
 
+@pytest.mark.parametrize("tup", [(2, 4, 64, 16, 32, 1, 1, 4), (4, 4, 32, 16, 32, 1, 2, 8)])
+def test_host_buffer_row_blocked_overlap_bitwise(cuda, tup):
+    """A >= 8 MB row-major: the host path overlaps row blocks (H2D of block
+    i+1 with the kernel of block i); every element still bit-equals the
+    reference executor on the whole matrix."""
+    inp = K.GemmInput(2600, 16, 1024, "f32")  # 10.6 MB of A, ragged last block
+    t = K.GemmTuning(*tup)
+    a, b = O.fill(4, inp.m * inp.k, inp.k * inp.n, "f32", True)
+    got = K.execute_gemm_host(inp, t, a, b, "parity")
+    assert bitwise_equal(got, O.execute_gemm(inp.m, inp.n, inp.k, False, False, t.values(), a, b))
+    fast = K.execute_gemm_host(inp, t, a, b, "fast")
+    # 1e-5 is the reference's bound for K <= 300 (test_backends.cpp:142); the
+    # fp32 rounding error of a K-long dot product grows with K
+    assert O.max_rel_error(fast, O.naive_gemm(inp.m, inp.n, inp.k, 0, 0, a, b)) < max(1e-5, 2e-8 * inp.k)
+
+
 def test_executor_validation(cuda):
     """test_backends.cpp:168-178."""
     inp = K.GemmInput(4, 4, 4)
