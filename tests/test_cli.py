@@ -145,3 +145,26 @@ def test_bench_exhaustive_matches_reference_infer(tmp_path):
         assert row["chosen"] == ref["chosen"]
         assert row["measured_gflops"] == ref["measured_gflops"]
         assert row["legal_space_size"] == ref["legal_space_size"]
+
+
+def test_conv_pipeline_matches_reference_bytes(tmp_path):
+    """calibrate --kind conv -> generate on the synthetic descriptor (the
+    reference defaults) and the conv_small bounds of the reference tests:
+    sampler JSON and CSV byte-identical to the reference library (golden
+    conv_small entries: seed 11 calibration, seed 5 generation of 300)."""
+    import dataclasses
+    from test_pipeline import CONV_SMALL
+    hw = tmp_path / "synthetic.json"
+    hw.write_text(json.dumps(dataclasses.asdict(K.HardwareDescriptor())))
+    bounds = tmp_path / "conv_small.json"
+    bounds.write_text(CONV_SMALL)
+    s, d = tmp_path / "sampler.json", tmp_path / "conv.csv"
+    assert run("calibrate", "--kind", "conv", "--hw", hw, "--bounds", bounds, "--seed", 11, "--out", s)[0] == 0
+    assert s.read_text().rstrip("\n") == GOLDEN["sampler"]["conv_small_json"].rstrip("\n")
+    g = GOLDEN["generate"]["conv_small"]
+    code, out, err = run("generate", "--hw", hw, "--bounds", bounds, "--sampler", s, "--shapes", TABLE,
+                         "--shape-fraction", g["fixed_fraction"], "--samples", g["n"], "--seed", g["seed"], "--out", d)
+    assert code == 0, err
+    assert hashlib.sha256(d.read_bytes()).hexdigest() == g["csv_sha256"]
+    code, out, _ = run("report", "--dataset", d)
+    assert code == 0 and f"rows: {g['n']}" in out
