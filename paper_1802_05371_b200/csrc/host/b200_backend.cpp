@@ -18,7 +18,7 @@ namespace {
 
 using dev::check;
 
-constexpr int kHostPipelineBlocks = 8;  // row blocks of the overlapped host-buffer GEMM (<= 8 events)
+constexpr int kHostPipelineBlocks = 4;  // row blocks of the overlapped host-buffer GEMM (<= 8 events)
 
 // Grow-only device allocation.
 struct DevBuf {
