@@ -296,6 +296,13 @@ KTUNE_API int ktune_select_gemm(const ktune_hw* hw, const char* bounds_json, con
                                 const char* cache_dir, const ktune_gemm_input* in, int32_t top_k,
                                 ktune_gemm_tuning* chosen, int32_t* source /* 0 memory, 1 file, 2 inferred */);
 
+/* ---- command line (replaces proj/tools/ktune.cpp:700-806) ------------------
+ * The `ktune` front end: argv[1] is the verb (calibrate | generate | train |
+ * infer | bench | report), the flags are the reference CLI's; returns the
+ * process exit code (0 success, 1 runtime failure, 2 usage error).  The
+ * bin/ktune_b200 executable is a stub around this entry point. */
+KTUNE_API int ktune_cli_main(int argc, char** argv);
+
 #ifdef __cplusplus
 }
 #endif

@@ -183,6 +183,7 @@ _SIGNATURES = {
     "ktune_cache_store": ([ctypes.c_char_p, ctypes.c_char_p], ctypes.c_int),
     "ktune_select_gemm": ([_P(HwC), ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, _P(GemmInputC),
                            ctypes.c_int32, _P(GemmTuningC), _P(ctypes.c_int32)], ctypes.c_int),
+    "ktune_cli_main": ([ctypes.c_int, _P(ctypes.c_char_p)], ctypes.c_int),
 }
 
 _lib = None

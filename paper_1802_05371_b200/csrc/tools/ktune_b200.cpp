@@ -38,6 +38,7 @@
 #include "ktune/sampling.hpp"
 #include "ktune/space.hpp"
 #include "ktune/tuner.hpp"
+#include "ktune_b200.h"
 
 namespace {
 
@@ -692,7 +693,7 @@ void usage() {
 // The CLI lives inside libktune_b200.so behind one C entry point, so the
 // executable (tools/ktune_main.c) is a few KB that links the library instead
 // of a second copy of every kernel; the C++ API stays hidden in the .so.
-extern "C" __attribute__((visibility("default"))) int ktune_cli_main(int argc, char** argv) {
+extern "C" KTUNE_API int ktune_cli_main(int argc, char** argv) {
     if (argc < 2) {
         usage();
         std::fprintf(stderr, "error: a subcommand is required\n");
