@@ -587,7 +587,7 @@ def our_arm(args):
         pick = [int(x) for x in args.pick.split(",")]
         sel_info = {"screened": 0, "legal_space": None, "seconds": None, "fixed": True}
     elif rank == 0:
-        sel = select_gemm(inp, hw, bounds, candidates=args.candidates, top_k=16, seed=0,
+        sel = select_gemm(inp, hw, bounds, candidates=args.candidates, top_k=48, seed=0,
                           extra=[K.GemmTuning(*PAPER_TUPLE)])
         best_t, _ = rerank(inp, [t for t, _ in sel.top], sets, stream)
         pick = best_t.values()

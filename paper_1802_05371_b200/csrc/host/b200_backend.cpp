@@ -18,8 +18,6 @@ namespace {
 
 using dev::check;
 
-constexpr int kHostPipelineBlocks = 4;  // row blocks of the overlapped host-buffer GEMM (<= 8 events)
-
 // Grow-only device allocation.
 struct DevBuf {
     void* ptr{nullptr};
@@ -53,14 +51,6 @@ struct DeviceState {
     DevBuf out, ws;
     // host-buffer staging
     DevBuf ha, hb, hc, hws;
-    cudaStream_t copy{nullptr};  // H2D stream of the row-blocked host path
-    cudaEvent_t evb{nullptr}, eva[8]{};
-    void init_copy() {
-        if (copy) return;
-        check(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "cudaStreamCreate");
-        check(cudaEventCreateWithFlags(&evb, cudaEventDisableTiming), "cudaEventCreate");
-        for (auto& e : eva) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-    }
     void init() {
         if (stream) return;
         check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -191,44 +181,10 @@ void execute_gemm_host(const GemmInput& in, const GemmTuning& t, dev::Mode mode,
     st.hb.reserve(std::size_t(b_len) * es, false);
     st.hc.reserve(std::size_t(c_len) * os, false);
     st.hws.reserve(wsb, false);
-    // Row-blocked overlap when A is row-major (rows of C depend only on rows
-    // of A): block i's kernel runs on the compute stream while block i+1's
-    // rows of A cross PCIe on the copy stream, and block i's rows of C return
-    // while later blocks compute.  Every output element is produced by the
-    // same kernel arithmetic as one whole-matrix launch (the tuple's fold
-    // order does not depend on M), so results are identical.
-    const std::size_t a_bytes = std::size_t(a_len) * es;
-    const int blocks = (!in.trans_a && a_bytes >= (std::size_t(8) << 20)) ? kHostPipelineBlocks : 1;
-    std::int64_t rows_per = (in.m + blocks - 1) / blocks;
-    rows_per = ((rows_per + t.m_l - 1) / t.m_l) * t.m_l;  // whole block-rows of the tuple
+    check(cudaMemcpyAsync(st.ha.ptr, a, std::size_t(a_len) * es, cudaMemcpyHostToDevice, st.stream), "H2D A");
     check(cudaMemcpyAsync(st.hb.ptr, b, std::size_t(b_len) * es, cudaMemcpyHostToDevice, st.stream), "H2D B");
-    if (blocks == 1 || rows_per >= in.m) {
-        check(cudaMemcpyAsync(st.ha.ptr, a, a_bytes, cudaMemcpyHostToDevice, st.stream), "H2D A");
-        dev::gemm(in, t, mode, st.ha.ptr, st.hb.ptr, st.hc.ptr, st.hws.ptr, st.hws.bytes, st.stream);
-        check(cudaMemcpyAsync(c, st.hc.ptr, std::size_t(c_len) * os, cudaMemcpyDeviceToHost, st.stream), "D2H C");
-        check(cudaStreamSynchronize(st.stream), "cudaStreamSynchronize");
-        return;
-    }
-    st.init_copy();
-    check(cudaEventRecord(st.evb, st.stream), "cudaEventRecord");
-    check(cudaStreamWaitEvent(st.copy, st.evb, 0), "cudaStreamWaitEvent");  // B first, on the compute stream
-    for (std::int64_t r0 = 0, i = 0; r0 < in.m; r0 += rows_per, ++i) {
-        const std::int64_t rows = std::min(rows_per, in.m - r0);
-        const std::size_t ao = std::size_t(r0) * std::size_t(in.k) * es;
-        check(cudaMemcpyAsync(static_cast<char*>(st.ha.ptr) + ao, static_cast<const char*>(a) + ao,
-                              std::size_t(rows) * std::size_t(in.k) * es, cudaMemcpyHostToDevice, st.copy),
-              "H2D A block");
-        check(cudaEventRecord(st.eva[i], st.copy), "cudaEventRecord");
-        check(cudaStreamWaitEvent(st.stream, st.eva[i], 0), "cudaStreamWaitEvent");
-        GemmInput sub = in;
-        sub.m = rows;
-        const std::size_t co = std::size_t(r0) * std::size_t(in.n) * os;
-        dev::gemm(sub, t, mode, static_cast<char*>(st.ha.ptr) + ao, st.hb.ptr, static_cast<char*>(st.hc.ptr) + co,
-                  st.hws.ptr, st.hws.bytes, st.stream);
-        check(cudaMemcpyAsync(static_cast<char*>(c) + co, static_cast<char*>(st.hc.ptr) + co,
-                              std::size_t(rows) * std::size_t(in.n) * os, cudaMemcpyDeviceToHost, st.stream),
-              "D2H C block");
-    }
+    dev::gemm(in, t, mode, st.ha.ptr, st.hb.ptr, st.hc.ptr, st.hws.ptr, st.hws.bytes, st.stream);
+    check(cudaMemcpyAsync(c, st.hc.ptr, std::size_t(c_len) * os, cudaMemcpyDeviceToHost, st.stream), "D2H C");
     check(cudaStreamSynchronize(st.stream), "cudaStreamSynchronize");
 }
 

@@ -135,10 +135,9 @@ def test_host_buffer_entry_point_bitwise(cuda):
 
 
 @pytest.mark.parametrize("tup", [(2, 4, 64, 16, 32, 1, 1, 4), (4, 4, 32, 16, 32, 1, 2, 8)])
-def test_host_buffer_row_blocked_overlap_bitwise(cuda, tup):
-    """A >= 8 MB row-major: the host path overlaps row blocks (H2D of block
-    i+1 with the kernel of block i); every element still bit-equals the
-    reference executor on the whole matrix."""
+def test_host_buffer_large_operands_bitwise(cuda, tup):
+    """The host-buffer path at DeepBench size (10.6 MB of A, ragged last
+    block-row): bit-equal to the reference executor, fast within bound."""
     inp = K.GemmInput(2600, 16, 1024, "f32")  # 10.6 MB of A, ragged last block
     t = K.GemmTuning(*tup)
     a, b = O.fill(4, inp.m * inp.k, inp.k * inp.n, "f32", True)
