@@ -314,13 +314,23 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                         float accv[32];
 #pragma unroll
                         for (int i = 0; i < 32; ++i) accv[i] = 0.f;
-                        for (int gg = 0; gg < p.nz - 1; ++gg) {
-                            const float* src = p.ws + gg * total + base;
-                            float part[32];
+                        // two slices per batch of in-flight loads, added in slice order
+                        constexpr int FB = 2;
+                        for (int g0 = 0; g0 < p.nz - 1; g0 += FB) {
+                            float part[FB][32];
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) part[i] = i < ncols ? __ldcg(src + i * p.PQN) : 0.f;
+                            for (int f = 0; f < FB; ++f) {
+                                const bool live = g0 + f < p.nz - 1;
+                                const float* src = p.ws + (g0 + f) * total + base;
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) accv[i] = __fadd_rn(accv[i], part[i]);
+                                for (int i = 0; i < 32; ++i)
+                                    part[f][i] = (live && i < ncols) ? __ldcg(src + i * p.PQN) : 0.f;
+                            }
+#pragma unroll
+                            for (int f = 0; f < FB; ++f)
+                                if (g0 + f < p.nz - 1)
+#pragma unroll
+                                    for (int i = 0; i < 32; ++i) accv[i] = __fadd_rn(accv[i], part[f][i]);
                         }
 #pragma unroll
                         for (int i = 0; i < 32; ++i) v[i] = __fadd_rn(accv[i], v[i]);
@@ -336,11 +346,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 }
             }
             if (!last && p.nz > 1) {
-                __threadfence();
+                // bar.sync orders the 128 threads' partial stores before one
+                // thread's cumulative gpu-scope release (no per-thread fence)
                 asm volatile("bar.sync 1, 128;\n" ::: "memory");
                 if (threadIdx.x == 64) {
                     unsigned long long* flag = p.flags + std::int64_t(w.g) * tiles + w.tile;
-                    asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(p.token) : "memory");
+                    asm volatile("fence.acq_rel.gpu;\nst.release.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(p.token)
+                                 : "memory");
                 }
             }
             if (++acc == p.nacc) {
