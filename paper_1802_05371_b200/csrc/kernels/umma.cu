@@ -13,7 +13,8 @@
 //
 // ISAAC tuple -> tensor-core tile (the legality formulas of param_space.cpp
 // stay the space definition; tc_plan() adds the launchability rules):
-//   m_l   BLOCK_M = UMMA_M (128; 256 = CTA pair is the next variant)
+//   m_l   BLOCK_M: 64 or 128 = UMMA_M of one CTA, 256 = a CTA pair
+//         (tcgen05.mma.cta_group::2, 128 rows per CTA)
 //   n_l   BLOCK_N = UMMA_N (16..256)
 //   u     BLOCK_K elements per pipeline stage (>= 32 bytes)
 //   k_g   split-K slices over the grid (deterministic ordered fix-up, as
@@ -319,8 +320,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int u = cta; u < n_units; u += ncta) {
             const Unit w = unit_of(p, u);
             const bool last = (w.g == p.nz - 1);
-            const int row = w.m0 + int(rank) * 128 + quarter * 32 + lane;
-            const bool row_ok = row < p.M && quarter * 32 + lane < (PAIR ? 128 : p.bm);
+            // accumulator row -> TMEM lane: M = 128 (and each CTA of a pair):
+            // row r in lane r; M = 64: rows 16q..16q+15 in lanes 32q..32q+15
+            // of warp quarter q (the upper 16 lanes of each quarter unused)
+            const int row = p.bm == 64 ? w.m0 + quarter * 16 + lane : w.m0 + int(rank) * 128 + quarter * 32 + lane;
+            const bool row_ok = row < p.M && (p.bm == 64 ? lane < 16 : true);
             // split-K flags are per CTA-half of a pair tile
             const std::int64_t ftile = PAIR ? (std::int64_t(w.tile / p.tiles_n) * 2 + rank) * p.tiles_n +
                                                   w.tile % p.tiles_n
@@ -511,8 +515,8 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     TcPlan pl;
     auto& p = pl.p;
     pl.kind = in.dtype == Dtype::tf32 ? 1 : 0;
-    if (t.m_l != 128 && t.m_l != 256)
-        throw unsupported_error("tensor-core family: m_l must be 128 (one CTA) or 256 (CTA pair), got " +
+    if (t.m_l != 64 && t.m_l != 128 && t.m_l != 256)
+        throw unsupported_error("tensor-core family: m_l must be 64 or 128 (one CTA) or 256 (CTA pair), got " +
                                 std::to_string(t.m_l));
     pl.pair = t.m_l == 256;
     if (pl.pair && (t.n_l < 32 || t.n_l % 32 != 0))
@@ -528,8 +532,8 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     p.M = int(in.m);
     p.N = int(in.n);
     p.K = int(in.k);
-    p.bm = 128;  // rows staged per CTA (a pair covers 256)
-    p.tile_m = pl.pair ? 256 : 128;
+    p.bm = t.m_l == 64 ? 64 : 128;  // rows staged per CTA (a pair covers 256); UMMA_M = 64 for m_l = 64
+    p.tile_m = pl.pair ? 256 : p.bm;
     p.bn = t.n_l;
     const int bn_cta = pl.pair ? t.n_l / 2 : t.n_l;  // B columns staged per CTA
     p.bk = t.u;
@@ -583,14 +587,14 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     pl.smem = extra + stage_bytes * std::size_t(stages);
     p.nacc = (t.k_s == 2 && 2 * p.bn <= 512) ? 2 : 1;
     p.tmem_cols = std::max(32, pow2_ceil(p.nacc * p.bn));
-    p.tiles_m = int(ceil_div(in.m, pl.pair ? 256 : 128));
+    p.tiles_m = int(ceil_div(in.m, p.tile_m));
     p.tiles_n = int(ceil_div(in.n, p.bn));
     p.raster = std::max(1, std::min(p.tiles_n, t.n_s));
     // instruction descriptor: F32 accumulate, operand formats, majors, N>>3, M>>4
     const unsigned fmt = in.dtype == Dtype::bf16 ? 1u : (in.dtype == Dtype::f16 ? 0u : 2u);
     p.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (unsigned(p.a_kmajor ? 0 : 1) << 15) |
               (unsigned(p.b_kmajor ? 0 : 1) << 16) | (unsigned(p.bn >> 3) << 17) |
-              (unsigned((pl.pair ? 256 : 128) >> 4) << 24);
+              (unsigned((pl.pair ? 256 : p.bm) >> 4) << 24);
     // Shared-memory matrix descriptors (tcgen05 "version 1"): high word =
     // SBO (8 rows x swizzle span) | version 1 | swizzle layout; LBO = 16 B for
     // K-major (unused with swizzle), = box stride between MN atoms for
