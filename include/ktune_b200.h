@@ -296,6 +296,16 @@ KTUNE_API int ktune_select_gemm(const ktune_hw* hw, const char* bounds_json, con
                                 const char* cache_dir, const ktune_gemm_input* in, int32_t top_k,
                                 ktune_gemm_tuning* chosen, int32_t* source /* 0 memory, 1 file, 2 inferred */);
 
+/* ---- KTN1 tensor files (replaces proj/src/tensor_file.cpp:36-112) -----------
+ * Same bytes as the reference writer: "KTN1", int32 element size, int32 rank,
+ * int64 dims, row-major payload; f32 / f64 only (others: INVALID_ARGUMENT). */
+KTUNE_API int ktune_tensor_write(const char* path, int32_t dtype, const int64_t* dims, int32_t ndims,
+                                 const void* data);
+/* Header into dtype / dims8[8] / ndims; the payload into data when
+ * data != NULL and cap (elements) covers it (call once with data = NULL to size). */
+KTUNE_API int ktune_tensor_read(const char* path, int32_t* dtype, int64_t* dims8, int32_t* ndims, void* data,
+                                int64_t cap);
+
 /* ---- command line (replaces proj/tools/ktune.cpp:700-806) ------------------
  * The `ktune` front end: argv[1] is the verb (calibrate | generate | train |
  * infer | bench | report), the flags are the reference CLI's; returns the

@@ -24,6 +24,7 @@
 #include "ktune/param_space.hpp"
 #include "ktune/perf_model.hpp"
 #include "ktune/pipeline.hpp"
+#include "ktune/tensor_file.hpp"
 #include "ktune/sampler.hpp"
 
 using namespace ktune;
@@ -504,6 +505,20 @@ __attribute__((visibility("default"))) int ref_infer_gemm_analytical(const char*
             AnalyticalPredictor pred(h);
             g_text = to_json_text(infer_gemm(pred, in, h, b, top_k, be));
         }
+    });
+}
+
+// --- KTN1 tensor files (tensor_file.cpp) ------------------------------------
+__attribute__((visibility("default"))) int ref_write_tensor(const char* path, int f64, const std::int64_t* dims,
+                                                            int ndims, const void* data) {
+    return guarded([&] {
+        TensorFile t;
+        t.dtype = f64 ? Dtype::f64 : Dtype::f32;
+        t.dims.assign(dims, dims + ndims);
+        const std::int64_t n = t.element_count();
+        if (f64) t.f64.assign(static_cast<const double*>(data), static_cast<const double*>(data) + n);
+        else t.f32.assign(static_cast<const float*>(data), static_cast<const float*>(data) + n);
+        write_tensor(path, t);
     });
 }
 

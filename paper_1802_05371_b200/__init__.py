@@ -25,7 +25,7 @@ __all__ = [
     "LegalityVerdict", "estimate_resources", "is_legal", "enumerate_legal", "encode_features",
     "build_indirection_table", "execute_gemm", "execute_conv", "execute_gemm_host", "execute_conv_host",
     "gemm_workspace_size", "conv_workspace_size", "measure", "B200Backend", "l2_flush", "KtuneError",
-    "InvalidArgument", "Unsupported", "WorkspaceTooSmall", "CudaError", "FIXTURES",
+    "InvalidArgument", "Unsupported", "WorkspaceTooSmall", "CudaError", "FIXTURES", "write_tensor", "read_tensor",
 ]
 
 FIXTURES = os.path.join(os.path.dirname(os.path.abspath(__file__)), "fixtures")
@@ -376,6 +376,28 @@ def execute_conv_host(inp: ConvInput, t: ConvTuning, images, filters, mode="pari
     _lib.call("ktune_execute_conv", ctypes.byref(inp.cstruct()), ctypes.byref(t.c()), _mode(mode),
               images.ctypes.data_as(ctypes.c_void_p), images.size, filters.ctypes.data_as(ctypes.c_void_p),
               filters.size, out.ctypes.data_as(ctypes.c_void_p), out.size)
+    return out
+
+
+def write_tensor(path: str, array) -> None:
+    """KTN1 file (write_tensor, tensor_file.cpp:36-69): f32 / f64 arrays."""
+    a = np.ascontiguousarray(array)
+    code = {np.dtype(np.float32): DTYPE_CODES["f32"], np.dtype(np.float64): DTYPE_CODES["f64"]}.get(a.dtype)
+    if code is None:
+        raise InvalidArgument(_lib.ERR_INVALID_ARGUMENT, f"{a.dtype} tensor files are not supported")
+    dims = (ctypes.c_int64 * max(1, a.ndim))(*a.shape)
+    _lib.call("ktune_tensor_write", os.fsencode(path), code, dims, a.ndim, a.ctypes.data_as(ctypes.c_void_p))
+
+
+def read_tensor(path: str) -> np.ndarray:
+    """KTN1 file -> numpy array of its dtype and shape (read_tensor, :71-112)."""
+    dt, nd = ctypes.c_int32(), ctypes.c_int32()
+    dims = (ctypes.c_int64 * 8)()
+    _lib.call("ktune_tensor_read", os.fsencode(path), ctypes.byref(dt), dims, ctypes.byref(nd), None, 0)
+    shape = tuple(dims[i] for i in range(nd.value))
+    out = np.empty(shape, np.float32 if DTYPE_NAMES[dt.value] == "f32" else np.float64)
+    _lib.call("ktune_tensor_read", os.fsencode(path), ctypes.byref(dt), dims, ctypes.byref(nd),
+              out.ctypes.data_as(ctypes.c_void_p), out.size)
     return out
 
 

@@ -184,6 +184,9 @@ _SIGNATURES = {
     "ktune_select_gemm": ([_P(HwC), ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, _P(GemmInputC),
                            ctypes.c_int32, _P(GemmTuningC), _P(ctypes.c_int32)], ctypes.c_int),
     "ktune_cli_main": ([ctypes.c_int, _P(ctypes.c_char_p)], ctypes.c_int),
+    "ktune_tensor_write": ([ctypes.c_char_p, ctypes.c_int32, _P(ctypes.c_int64), ctypes.c_int32, _vp], ctypes.c_int),
+    "ktune_tensor_read": ([ctypes.c_char_p, _P(ctypes.c_int32), _P(ctypes.c_int64), _P(ctypes.c_int32), _vp,
+                           ctypes.c_int64], ctypes.c_int),
 }
 
 _lib = None

@@ -10,6 +10,7 @@
 #include <string>
 
 #include "capi_internal.hpp"
+#include "ktune/tensor_file.hpp"
 
 using namespace ktune;
 
@@ -229,6 +230,39 @@ int ktune_measure_conv(const ktune_hw* hw, const ktune_conv_input* in, const ktu
 
 int ktune_l2_flush(void* stream) {
     return guard([&] { dev::l2_flush(static_cast<cudaStream_t>(stream)); });
+}
+
+int ktune_tensor_write(const char* path, int32_t dtype, const int64_t* dims, int32_t ndims, const void* data) {
+    return guard([&] {
+        need(path, "path");
+        TensorFile t;
+        t.dtype = dtype_of(dtype);
+        if (ndims < 0 || (ndims > 0 && dims == nullptr)) throw std::invalid_argument("tensor_write: bad dims");
+        t.dims.assign(dims, dims + ndims);
+        const std::int64_t n = ndims > 0 ? t.element_count() : 0;
+        if (n > 0) need(data, "data");
+        if (t.dtype == Dtype::f32) t.f32.assign(static_cast<const float*>(data), static_cast<const float*>(data) + n);
+        else if (t.dtype == Dtype::f64) t.f64.assign(static_cast<const double*>(data), static_cast<const double*>(data) + n);
+        write_tensor(path, t);
+    });
+}
+
+int ktune_tensor_read(const char* path, int32_t* dtype, int64_t* dims8, int32_t* ndims, void* data, int64_t cap) {
+    return guard([&] {
+        need(path, "path");
+        need(dtype, "dtype");
+        need(dims8, "dims");
+        need(ndims, "ndims");
+        const TensorFile t = read_tensor(path);
+        *dtype = int32_t(t.dtype);
+        *ndims = int32_t(t.dims.size());
+        for (std::size_t i = 0; i < t.dims.size(); ++i) dims8[i] = t.dims[i];
+        const std::int64_t n = t.element_count();
+        if (data != nullptr && cap >= n) {
+            if (t.dtype == Dtype::f32) std::memcpy(data, t.f32.data(), std::size_t(n) * 4);
+            else std::memcpy(data, t.f64.data(), std::size_t(n) * 8);
+        }
+    });
 }
 
 }  // extern "C"
