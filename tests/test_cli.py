@@ -168,3 +168,35 @@ def test_conv_pipeline_matches_reference_bytes(tmp_path):
     assert hashlib.sha256(d.read_bytes()).hexdigest() == g["csv_sha256"]
     code, out, _ = run("report", "--dataset", d)
     assert code == 0 and f"rows: {g['n']}" in out
+
+
+@pytest.mark.parametrize("kind,dtype,bounds,fixture", [
+    ("gemm", "f32", "gemm_b200.json", "gemm_b200.json"),
+    ("conv", "f32", "conv_b200.json", "conv_b200.json"),
+    ("gemm", "bf16", "gemm_b200_tc.json", "gemm_b200_tc_bf16.json"),
+    ("conv", "bf16", "conv_b200_tc.json", "conv_b200_tc_bf16.json")])
+def test_calibrated_b200_sampler_fixtures(tmp_path, kind, dtype, bounds, fixture):
+    """fixtures/samplers/*: the calibrated samplers of the B200 spaces
+    (section 8(f) row 4) are what `calibrate --seed 11` produces, and the
+    f32 ones equal the reference library's calibration of the same space."""
+    out = tmp_path / "s.json"
+    b = os.path.join(K.FIXTURES, "bounds", bounds)
+    assert run("calibrate", "--kind", kind, "--dtype", dtype, "--hw", HW, "--bounds", b, "--seed", 11,
+               "--out", out)[0] == 0
+    want = open(os.path.join(K.FIXTURES, "samplers", fixture)).read()
+    assert out.read_text() == want
+    lib = O.reference()
+    if lib is None or dtype != "f32":
+        return
+    import ctypes
+    hw_json, bounds_json = open(HW).read().encode(), open(b).read().encode()
+    if kind == "gemm":
+        rc = lib.ref_calibrate_gemm(hw_json, bounds_json, ctypes.c_int64(512), ctypes.c_int64(512),
+                                    ctypes.c_int64(512), 1, ctypes.c_int64(100000), ctypes.c_uint64(11),
+                                    ctypes.c_double(100.0))
+    else:
+        d = (ctypes.c_int64 * 7)(16, 24, 240, 32, 16, 3, 3)
+        rc = lib.ref_calibrate_conv(hw_json, bounds_json, d, 1, ctypes.c_int64(100000), ctypes.c_uint64(11),
+                                    ctypes.c_double(100.0))
+    assert rc == 0
+    assert want.rstrip("\n") == lib.ref_last_text().decode().rstrip("\n")
