@@ -200,3 +200,17 @@ def test_calibrated_b200_sampler_fixtures(tmp_path, kind, dtype, bounds, fixture
                                     ctypes.c_double(100.0))
     assert rc == 0
     assert want.rstrip("\n") == lib.ref_last_text().decode().rstrip("\n")
+
+
+def test_fitted_b200_descriptor_loads_and_keeps_the_limits(tmp_path):
+    """fixtures/hw/b200_fitted.json (section 8(f) row 2) is a strict
+    descriptor: it loads, and only the four cost constants differ from the
+    nominal B200 descriptor (legality is the hardware's)."""
+    fitted = json.load(open(os.path.join(K.FIXTURES, "hw", "b200_fitted.json")))
+    nominal = json.load(open(HW))
+    assert set(fitted) == set(nominal)
+    assert {k for k in nominal if fitted[k] != nominal[k]} <= {"alu_latency", "alu_throughput", "mem_latency",
+                                                                "mem_throughput"}
+    out = tmp_path / "s.json"
+    assert run("calibrate", "--hw", os.path.join(K.FIXTURES, "hw", "b200_fitted.json"), "--bounds", GEMM_BOUNDS,
+               "--draws", 1000, "--trials", 100, "--out", out)[0] == 0
