@@ -362,9 +362,15 @@ Plan conv_plan(const ConvInput& in, const ConvTuning& t, const void* img = nullp
     auto va = [&](int, std::int64_t) { return vec_width(es, {in.k_filters}, {flt}, t.k_l); };
     // gather chunks must be whole n-runs: n_l and N multiples of the width
     auto vb = [&](int, std::int64_t) { return vec_width(es, {in.n_batch}, {img}, t.n_l); };
-    return plan_simt(in.k_filters, in.c * in.r * in.s, in.k_filters * in.p * in.q * in.n_batch, col_tiles, t.k_l,
-                     t.p_l * t.q_l * t.n_l, t.k_s, t.p_s * t.q_s * t.n_s, t.c_s, t.c_l, t.c_g, t.u, es, false, false,
-                     va, vb);
+    Plan pl = plan_simt(in.k_filters, in.c * in.r * in.s, in.k_filters * in.p * in.q * in.n_batch, col_tiles, t.k_l,
+                        t.p_l * t.q_l * t.n_l, t.k_s, t.p_s * t.q_s * t.n_s, t.c_s, t.c_l, t.c_g, t.u, es, false, false,
+                        va, vb);
+    // Precomputed chunk state for the filter operand (affine in the
+    // reduction index); the image gather keeps the tap decomposition.
+    const std::int64_t a_total = std::int64_t(pl.p.kl) << (pl.p.lml + pl.p.lw - pl.p.lva);
+    pl.p.fast_ld = ceil_div(a_total, pl.threads) <= ktune_dev::kChunkMax &&
+                   in.c * in.r * in.s * in.k_filters < (std::int64_t(1) << 31);
+    return pl;
 }
 
 template <typename T>

@@ -84,7 +84,8 @@ struct ChunkLd {
 // ---- GEMM policy: A is M x K (K x M when ta), B is K x N (N x K when tb) ----
 template <typename T>
 struct GemmProblem {
-    static constexpr bool kAffine = true;
+    static constexpr bool kAffine = true;   // both operands affine in the reduction index
+    static constexpr bool kAffineA = true;
     const T* a;
     const T* b;
     std::int64_t M, N, K;
@@ -120,7 +121,8 @@ struct GemmProblem {
 // with off(t) the indirection-table offset of backends.cpp:197-216.
 template <typename T>
 struct ConvProblem {
-    static constexpr bool kAffine = false;
+    static constexpr bool kAffine = false;  // the image gather is not (tap decomposition)
+    static constexpr bool kAffineA = true;  // the filters are: flt + t*K + row
     const T* flt;
     const T* img;
     std::int64_t Nb, P, Q, K, C, R, S, H, W;
@@ -130,6 +132,7 @@ struct ConvProblem {
     // chunk is entirely valid or entirely outside the tensor.
     __device__ int b_cols_valid(std::int64_t base, int v) const { return base < 0 ? 0 : v; }
     __device__ const T* a_addr(std::int64_t row, std::int64_t t) const { return flt + t * K + row; }
+    __device__ std::int64_t a_kstride() const { return K; }
     // t = (c*R + r)*S + s -> image offset of the tap (the indirection table
     // entry of backends.cpp:197-216).  The reduction index fits in 32 bits
     // (host-checked), so the decomposition uses 32-bit divisions: the 64-bit
@@ -341,10 +344,10 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads : LaunchCap<MS_, NS_, 
     ChunkLd ca[kChunkMax], cb[kChunkMax];
     int nca = 0, ncb = 0;
     std::int64_t a_wk = 0, b_wk = 0;  // element advance of one step
-    if constexpr (Prob::kAffine) {
+    const T* a_origin = prob.a_addr(0, 0);
+    if constexpr (Prob::kAffineA) {
         if (p.fast_ld) {
             a_wk = std::int64_t(p.w) * prob.a_kstride();
-            b_wk = std::int64_t(p.w) * prob.b_kstride();
             {
                 const int VA = 1 << p.lva;
                 const int lchunks = p.lml + p.lw - p.lva;
@@ -366,12 +369,17 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads : LaunchCap<MS_, NS_, 
                     const std::int64_t t0 = glo + kk;
                     const std::int64_t row = row0 + ii;
                     const bool rv = row < p.rows;
-                    ca[i].off = rv ? int(prob.a_addr(row, t0) - prob.a) : 0;
+                    ca[i].off = rv ? int(prob.a_addr(row, t0) - a_origin) : 0;
                     ca[i].dst = gx * p.a_group + (ARM ? ii * p.a_ld + kk : kk * p.a_ld + ii);
                     ca[i].lim = int(ghi - t0);
                     ca[i].cnt = ARM ? (rv ? VA : 0) : int(max(std::int64_t(0), min(std::int64_t(VA), p.rows - row)));
                 }
             }
+        }
+    }
+    if constexpr (Prob::kAffine) {
+        if (p.fast_ld) {
+            b_wk = std::int64_t(p.w) * prob.b_kstride();
             {
                 const int VB = 1 << p.lvb;
                 const int lchunks = p.lnl + p.lw - p.lvb;
@@ -400,8 +408,8 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads : LaunchCap<MS_, NS_, 
             }
         }
     }
-    auto load_fast = [&]<int BA, int BB>(std::int64_t st, T* dst) {
-        if constexpr (Prob::kAffine) {
+    auto load_fast_a = [&]<int BA>(std::int64_t st, T* dst) {
+        if constexpr (Prob::kAffineA) {
             const int dk = int(st) * p.w;
             const T* dummy = reinterpret_cast<const T*>(p.out);
 #pragma unroll
@@ -409,10 +417,17 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads : LaunchCap<MS_, NS_, 
                 if (i < nca) {
                     const int r = ca[i].lim - dk;
                     const int n = ARM ? min(max(r, 0), ca[i].cnt) : (r > 0 ? ca[i].cnt : 0);
-                    const T* src = n > 0 ? prob.a + (ca[i].off + st * a_wk) : dummy;
+                    const T* src = n > 0 ? a_origin + (ca[i].off + st * a_wk) : dummy;
                     cp_async_zfill<BA>(dst + ca[i].dst, src, n * int(sizeof(T)));
                 }
             }
+        }
+    };
+    auto load_fast = [&]<int BA, int BB>(std::int64_t st, T* dst) {
+        if constexpr (Prob::kAffine) {
+            const int dk = int(st) * p.w;
+            const T* dummy = reinterpret_cast<const T*>(p.out);
+            load_fast_a.template operator()<BA>(st, dst);
 #pragma unroll
             for (int i = 0; i < kChunkMax; ++i) {
                 if (i < ncb) {
@@ -442,10 +457,18 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads : LaunchCap<MS_, NS_, 
                 return;
             }
         }
-        switch (int(sizeof(T)) << p.lva) {
-            case 16: load_a.template operator()<16>(st, dst); break;
-            case 8: load_a.template operator()<8>(st, dst); break;
-            default: load_a.template operator()<int(sizeof(T))>(st, dst); break;
+        if (Prob::kAffineA && p.fast_ld) {
+            switch (int(sizeof(T)) << p.lva) {
+                case 16: load_fast_a.template operator()<16>(st, dst); break;
+                case 8: load_fast_a.template operator()<8>(st, dst); break;
+                default: load_fast_a.template operator()<int(sizeof(T))>(st, dst); break;
+            }
+        } else {
+            switch (int(sizeof(T)) << p.lva) {
+                case 16: load_a.template operator()<16>(st, dst); break;
+                case 8: load_a.template operator()<8>(st, dst); break;
+                default: load_a.template operator()<int(sizeof(T))>(st, dst); break;
+            }
         }
         switch (int(sizeof(T)) << p.lvb) {
             case 16: load_b.template operator()<16>(st, dst + p.a_stage); break;
