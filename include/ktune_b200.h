@@ -150,8 +150,17 @@ KTUNE_API int ktune_build_indirection_table(const ktune_conv_input* in, int64_t*
 
 /* ---- device kernels (replace execute_gemm / execute_conv, backends.cpp:228-444) */
 /* Workspace for k_g / c_g partials (0 bytes when the reduction is not split
- * across the grid).  No initialisation is needed: publication flags carry a
- * token unique to each launch.  One launch at a time per workspace. */
+ * across the grid): a 1 MiB region of per-tile arrival counters, then the
+ * partials of every slice; the slice that arrives last folds them in slice
+ * order and resets its counter.  The counter region (the first 1 MiB) must be
+ * zero before a workspace's first use -- allocate with cudaMemset 0 -- and
+ * every launch leaves it zero.  One launch at a time per workspace. */
+/* Launch geometry the library would use for this input/tuning (no launch):
+ * threads per block, dynamic shared memory, grid {x, y, z}, and the kernel
+ * family ("simt", "simt-tma", "simt-generic", "tcgen05", "tcgen05-pair"),
+ * NUL-terminated into family[0..family_cap).  Reporting aid for tools. */
+KTUNE_API int ktune_gemm_launch_info(const ktune_gemm_input* in, const ktune_gemm_tuning* t, int mode, int* threads,
+                                     size_t* smem_bytes, int* grid3, char* family, size_t family_cap);
 KTUNE_API int ktune_gemm_workspace_size(const ktune_gemm_input* in, const ktune_gemm_tuning* t, size_t* bytes);
 KTUNE_API int ktune_conv_workspace_size(const ktune_conv_input* in, const ktune_conv_tuning* t, size_t* bytes);
 /* C = op(A) op(B) on device buffers (row-major; A M x K or K x M when

@@ -283,6 +283,15 @@ def gemm_workspace_size(inp: GemmInput, t: GemmTuning) -> int:
     return n.value
 
 
+def gemm_launch_info(inp: GemmInput, t: GemmTuning, mode="fast") -> dict:
+    """Launch geometry and kernel family the library uses (no launch)."""
+    th, sm, grid = ctypes.c_int(), ctypes.c_size_t(), (ctypes.c_int * 3)()
+    fam = ctypes.create_string_buffer(64)
+    _lib.call("ktune_gemm_launch_info", ctypes.byref(inp.c()), ctypes.byref(t.c()), _mode(mode), ctypes.byref(th),
+              ctypes.byref(sm), grid, fam, 64)
+    return {"threads": th.value, "smem": sm.value, "grid": list(grid), "family": fam.value.decode()}
+
+
 def conv_workspace_size(inp: ConvInput, t: ConvTuning) -> int:
     n = ctypes.c_size_t()
     _lib.call("ktune_conv_workspace_size", ctypes.byref(inp.cstruct()), ctypes.byref(t.c()), ctypes.byref(n))
@@ -290,17 +299,26 @@ def conv_workspace_size(inp: ConvInput, t: ConvTuning) -> int:
 
 
 _workspaces: dict = {}
+_retired: list = []
 
 
-def _workspace(device, nbytes: int):
-    """Grow-only workspace per device (no initialisation needed)."""
+def _workspace(device, nbytes: int, stream=None):
+    """Grow-only workspace per (device, stream), zero-initialised (the split-K
+    counter region must start at zero; launches leave it zero).  A launch on
+    another stream never shares counters or partials with this one, and a
+    grown-out buffer is kept alive (work still in flight on the stream, or a
+    captured CUDA graph, may reference it)."""
     import torch
     if nbytes == 0:
         return None, 0
-    key = torch.device(device).index
+    key = (torch.device(device).index, int(stream or 0))
     ws = _workspaces.get(key)
     if ws is None or ws.numel() < nbytes:
-        ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        if ws is not None:
+            _retired.append(ws)
+        ws = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+        if not torch.cuda.is_current_stream_capturing():
+            torch.cuda.current_stream(device).synchronize()  # zeroed before any stream uses it
         _workspaces[key] = ws
     return ws, ws.numel()
 
@@ -330,8 +348,8 @@ def execute_gemm(inp: GemmInput, t: GemmTuning, a, b, c=None, mode="parity", str
     if c is None:
         c = torch.empty(inp.m * inp.n, dtype=getattr(torch, _TORCH_DT[out_dt]), device=a.device)
     _check_tensor(c, inp.m * inp.n, out_dt, "c")
-    ws, wsb = _workspace(a.device, gemm_workspace_size(inp, t))
     s = stream if stream is not None else torch.cuda.current_stream(a.device).cuda_stream
+    ws, wsb = _workspace(a.device, gemm_workspace_size(inp, t), s)
     _lib.call("ktune_gemm", ctypes.byref(inp.c()), ctypes.byref(t.c()), _mode(mode), a.data_ptr(), b.data_ptr(),
               c.data_ptr(), None if ws is None else ws.data_ptr(), wsb, s)
     return c
@@ -346,8 +364,8 @@ def execute_conv(inp: ConvInput, t: ConvTuning, images, filters, outputs=None, m
     if outputs is None:
         outputs = torch.empty(no, dtype=getattr(torch, _TORCH_DT[out_dt]), device=images.device)
     _check_tensor(outputs, no, out_dt, "outputs")
-    ws, wsb = _workspace(images.device, conv_workspace_size(inp, t))
     s = stream if stream is not None else torch.cuda.current_stream(images.device).cuda_stream
+    ws, wsb = _workspace(images.device, conv_workspace_size(inp, t), s)
     _lib.call("ktune_conv", ctypes.byref(inp.cstruct()), ctypes.byref(t.c()), _mode(mode), images.data_ptr(),
               filters.data_ptr(), outputs.data_ptr(), None if ws is None else ws.data_ptr(), wsb, s)
     return outputs

@@ -128,6 +128,8 @@ _SIGNATURES = {
     "ktune_encode_features_conv": ([_P(ConvInputC), _P(ConvTuningC), _vp], ctypes.c_int),
     "ktune_build_indirection_table": ([_P(ConvInputC), _vp, _i64, _P(_i64)], ctypes.c_int),
     "ktune_gemm_workspace_size": ([_P(GemmInputC), _P(GemmTuningC), _P(ctypes.c_size_t)], ctypes.c_int),
+    "ktune_gemm_launch_info": ([_P(GemmInputC), _P(GemmTuningC), ctypes.c_int, _P(ctypes.c_int), _P(ctypes.c_size_t),
+                                _P(ctypes.c_int), ctypes.c_char_p, ctypes.c_size_t], ctypes.c_int),
     "ktune_conv_workspace_size": ([_P(ConvInputC), _P(ConvTuningC), _P(ctypes.c_size_t)], ctypes.c_int),
     "ktune_gemm": ([_P(GemmInputC), _P(GemmTuningC), ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp],
                    ctypes.c_int),

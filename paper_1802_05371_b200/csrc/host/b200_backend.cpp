@@ -29,7 +29,10 @@ struct DevBuf {
         bytes = 0;
         check(cudaMalloc(&ptr, std::max<std::size_t>(n, 256)), "cudaMalloc");
         bytes = std::max<std::size_t>(n, 256);
-        if (zero) check(cudaMemset(ptr, 0, bytes), "cudaMemset");
+        if (zero) {
+            check(cudaMemset(ptr, 0, bytes), "cudaMemset");
+            check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");  // visible to non-blocking streams
+        }
     }
 };
 
@@ -128,7 +131,7 @@ MeasureResult measure_gemm_device(const HardwareDescriptor& hw, const GemmInput&
     const void* b = operand(st, 1, in.dtype, in.k * in.n, opt.seed);
     st.out.reserve(std::size_t(in.m * in.n) * output_elem_size(in.dtype), false);
     const std::size_t wsb = dev::gemm_workspace_bytes(in, t);
-    st.ws.reserve(wsb, false);
+    st.ws.reserve(wsb, true);  // split-K counter region must start zeroed
     const double flops = 2.0 * double(in.m) * double(in.n) * double(in.k);
     return time_it(st, opt, flops, [&] {
         dev::gemm(in, t, opt.mode, a, b, st.out.ptr, st.ws.ptr, st.ws.bytes, st.stream);
@@ -145,7 +148,7 @@ MeasureResult measure_conv_device(const HardwareDescriptor& hw, const ConvInput&
     const void* flt = operand(st, 1, in.dtype, in.c * in.r * in.s * in.k_filters, opt.seed);
     st.out.reserve(std::size_t(in.k_filters * in.p * in.q * in.n_batch) * output_elem_size(in.dtype), false);
     const std::size_t wsb = dev::conv_workspace_bytes(in, t);
-    st.ws.reserve(wsb, false);
+    st.ws.reserve(wsb, true);  // split-K counter region must start zeroed
     const double flops = 2.0 * double(in.n_batch) * double(in.p) * double(in.q) * double(in.k_filters) *
                          double(in.c) * double(in.r) * double(in.s);
     return time_it(st, opt, flops, [&] {
@@ -180,7 +183,7 @@ void execute_gemm_host(const GemmInput& in, const GemmTuning& t, dev::Mode mode,
     st.ha.reserve(std::size_t(a_len) * es, false);
     st.hb.reserve(std::size_t(b_len) * es, false);
     st.hc.reserve(std::size_t(c_len) * os, false);
-    st.hws.reserve(wsb, false);
+    st.hws.reserve(wsb, true);
     check(cudaMemcpyAsync(st.ha.ptr, a, std::size_t(a_len) * es, cudaMemcpyHostToDevice, st.stream), "H2D A");
     check(cudaMemcpyAsync(st.hb.ptr, b, std::size_t(b_len) * es, cudaMemcpyHostToDevice, st.stream), "H2D B");
     dev::gemm(in, t, mode, st.ha.ptr, st.hb.ptr, st.hc.ptr, st.hws.ptr, st.hws.bytes, st.stream);
@@ -203,7 +206,7 @@ void execute_conv_host(const ConvInput& in, const ConvTuning& t, dev::Mode mode,
     st.ha.reserve(std::size_t(img_len) * es, false);
     st.hb.reserve(std::size_t(flt_len) * es, false);
     st.hc.reserve(std::size_t(out_len) * os, false);
-    st.hws.reserve(wsb, false);
+    st.hws.reserve(wsb, true);
     check(cudaMemcpyAsync(st.ha.ptr, img, std::size_t(img_len) * es, cudaMemcpyHostToDevice, st.stream), "H2D images");
     check(cudaMemcpyAsync(st.hb.ptr, flt, std::size_t(flt_len) * es, cudaMemcpyHostToDevice, st.stream), "H2D filters");
     dev::conv(in, t, mode, st.ha.ptr, st.hb.ptr, st.hc.ptr, st.hws.ptr, st.hws.bytes, st.stream);

@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstring>
 #include <string>
 
@@ -165,6 +166,24 @@ int ktune_conv_workspace_size(const ktune_conv_input* in, const ktune_conv_tunin
     return guard([&] {
         need(bytes, "bytes");
         *bytes = dev::conv_workspace_bytes(conv_in(in), conv_t(t));
+    });
+}
+
+int ktune_gemm_launch_info(const ktune_gemm_input* in, const ktune_gemm_tuning* t, int mode, int* threads,
+                           size_t* smem_bytes, int* grid3, char* family, size_t family_cap) {
+    return guard([&] {
+        need(threads, "threads");
+        need(smem_bytes, "smem_bytes");
+        need(grid3, "grid3");
+        const dev::LaunchInfo li = dev::gemm_launch_info(conv_in(in), conv_t(t), mode_of(mode));
+        *threads = li.threads;
+        *smem_bytes = li.smem_bytes;
+        grid3[0] = li.grid_x;
+        grid3[1] = li.grid_y;
+        grid3[2] = li.grid_z;
+        if (family != nullptr && family_cap > 0) {
+            std::snprintf(family, family_cap, "%s%s", li.family, li.generic ? "-generic" : "");
+        }
     });
 }
 

@@ -42,10 +42,13 @@ enum class Mode : int {
 };
 
 // Bytes of workspace a launch needs (0 when k_g splits collapse to one
-// slice): per-(slice, tile) publication flags followed by the partial tiles
-// of slices 0..nz-2.  Flags carry a token unique to each launch, so the
-// workspace needs no initialisation and can be reused freely (one launch at a
-// time per workspace).
+// slice).  Every split workspace starts with a kSplitCounterBytes region of
+// 32-bit arrival counters (one per output tile, SIMT family: the slice that
+// arrives last folds all partials in slice order and resets its counter), so
+// that region must be ZERO before a workspace's first use; every launch
+// leaves it zero.  Partial tiles and the tensor-core family's token flags
+// live after it.  One launch at a time per workspace.
+constexpr std::size_t kSplitCounterBytes = std::size_t(1) << 20;
 std::size_t gemm_workspace_bytes(const GemmInput& in, const GemmTuning& t);
 std::size_t conv_workspace_bytes(const ConvInput& in, const ConvTuning& t);
 

@@ -26,7 +26,9 @@
 #include "ktune/kernels.hpp"
 #include "simt.cuh"
 #include "simt_tiles.cuh"
+#include "simt_tma.cuh"
 #include "umma.hpp"
+#include "umma_common.cuh"
 
 namespace ktune {
 namespace dev {
@@ -218,10 +220,15 @@ Plan plan_simt(std::int64_t rows, std::int64_t red, std::int64_t out_elems, std:
     pl.ns = ns;
     pl.ks = ks;
     if (p.nz > 1) {
-        pl.counter_bytes =
-            (std::size_t(pl.col_tiles) * pl.row_tiles * std::size_t(p.nz - 1) * sizeof(unsigned long long) + 255) /
-            256 * 256;
-        pl.ws_bytes = pl.counter_bytes + std::size_t(p.nz - 1) * std::size_t(out_elems) * std::size_t(esize);
+        // one arrival counter per output tile in the zeroed counter region,
+        // then the partial tensors of all nz slices (whichever slice arrives
+        // last folds them; simt.cuh)
+        const std::size_t tiles = std::size_t(pl.col_tiles) * std::size_t(pl.row_tiles);
+        if (tiles * sizeof(unsigned) > kSplitCounterBytes)
+            throw unsupported_error("k_g > 1 with " + std::to_string(tiles) + " output tiles exceeds the " +
+                                    std::to_string(kSplitCounterBytes / sizeof(unsigned)) + " split-K counters");
+        pl.counter_bytes = kSplitCounterBytes;
+        pl.ws_bytes = pl.counter_bytes + std::size_t(p.nz) * std::size_t(out_elems) * std::size_t(esize);
     }
     return pl;
 }
@@ -373,6 +380,156 @@ Plan conv_plan(const ConvInput& in, const ConvTuning& t, const void* img = nullp
     return pl;
 }
 
+// ---- K1t: the TMA-fed variant (simt_tma.cuh) ------------------------------
+// Eligible: fp32, a compiled NARROW register tile with vector reads along the
+// reduction (w % 4 == 0, k_s | 4), <= 256 compute threads, every box
+// dimension <= 256, 16-byte aligned operands and leading dimensions (TMA).
+// Everything else runs the cp.async kernel; both give identical results.
+const void* tma_lookup(bool par, bool arm, bool brm, int ms, int ns, int ks) {
+    using namespace ktune_dev;
+    using L = const void* (*)(int, int, int);
+    const int lay = (arm ? 0 : 1) + (brm ? 2 : 0);  // nn, tn, nt, tt
+    static const L fp[] = {&simt_tma_f32_parity_nn, &simt_tma_f32_parity_tn, &simt_tma_f32_parity_nt,
+                           &simt_tma_f32_parity_tt};
+    static const L ff[] = {&simt_tma_f32_fast_nn, &simt_tma_f32_fast_tn, &simt_tma_f32_fast_nt, &simt_tma_f32_fast_tt};
+    return (par ? fp : ff)[lay](ms, ns, ks);
+}
+
+struct TmaLaunch {
+    const void* kernel{nullptr};
+    ktune_dev::TmaGeom g{};
+    int threads{0};
+    std::size_t smem{0};
+    int stages{0};
+};
+
+// KTUNE_SIMT_TMA=0 selects the cp.async kernel (read per launch, so tests can
+// compare both feeds in one process).
+bool tma_enabled() {
+    const char* e = std::getenv("KTUNE_SIMT_TMA");
+    return !(e != nullptr && e[0] == '0');
+}
+
+std::size_t round_up(std::size_t x, std::size_t a) { return (x + a - 1) / a * a; }
+
+// Geometry of the TMA variant, or kernel == nullptr when not eligible.
+TmaLaunch tma_geometry(const GemmInput& in, const Plan& pl, Mode mode, const void* a, const void* b) {
+    TmaLaunch tl;
+    const auto& p = pl.p;
+    if (!tma_enabled() || in.dtype != Dtype::f32 || pl.generic) return tl;
+    constexpr int es = 4, vk = 4;
+    if (pl.threads > ktune_dev::kNarrowThreads || p.w % vk != 0 || vk % pl.ks != 0) return tl;
+    if (p.ml > 256 || p.nl > 256 || p.w > 256) return tl;
+    auto aligned = [](const void* q) { return (reinterpret_cast<std::uintptr_t>(q) & 15u) == 0; };
+    if (!aligned(a) || !aligned(b)) return tl;
+    const bool arm = pl.arm, brm = pl.brm;
+    // leading dimensions (elements) of the row-major views TMA walks
+    const std::int64_t lda = arm ? in.k : in.m, ldb = brm ? in.k : in.n;
+    if (lda % vk != 0 || ldb % vk != 0) return tl;
+    if ((!arm && p.ml % vk != 0) || (!brm && p.nl % vk != 0)) return tl;
+    // k-contiguous boxes must start on 16-byte boundaries: every k_g / k_l
+    // slice start a multiple of 4 (the planner's 16-byte vector width)
+    if ((arm && p.lva != 2) || (brm && p.lvb != 2)) return tl;
+    if (in.m >= (std::int64_t(1) << 31) || in.n >= (std::int64_t(1) << 31) || in.k >= (std::int64_t(1) << 31)) return tl;
+    tl.kernel = tma_lookup(mode == Mode::parity, arm, brm, pl.ms, pl.ns, pl.ks);
+    if (tl.kernel == nullptr) return tl;
+    auto& g = tl.g;
+    auto side = [&](bool kc, int rows, int& box_bytes, int& stride, int& nbox, int& wb, int& rb, int& grp) {
+        if (kc) {  // [rows][w] split into 128-byte-wide swizzled boxes
+            wb = std::min(p.w, 128 / es);
+            nbox = p.w / wb;
+            rb = wb * es;
+            box_bytes = rows * wb * es;
+            stride = int(round_up(std::size_t(box_bytes), rb > 16 ? 1024 : 128));
+        } else {   // [w][rows], dense, no swizzle
+            wb = p.w;
+            nbox = 1;
+            rb = 16;
+            box_bytes = rows * p.w * es;
+            stride = int(round_up(std::size_t(box_bytes), 128));
+        }
+        grp = nbox * stride;
+    };
+    side(arm, p.ml, g.a_box_bytes, g.a_box_stride, g.a_nbox, g.a_wb, g.a_rb, g.a_grp);
+    side(brm, p.nl, g.b_box_bytes, g.b_box_stride, g.b_nbox, g.b_wb, g.b_rb, g.b_grp);
+    g.a_lwb = ilog2(g.a_wb);
+    g.b_lwb = ilog2(g.b_wb);
+    // group regions keep 1024-byte alignment for the swizzled boxes that follow
+    g.a_grp = int(round_up(std::size_t(g.a_grp), 1024));
+    g.b_grp = int(round_up(std::size_t(g.b_grp), 1024));
+    g.stage_bytes = p.kl * (g.a_grp + g.b_grp);
+    g.compute_threads = pl.threads;
+    g.producer_warp = (pl.threads + 31) / 32;
+    tl.threads = g.producer_warp * 32 + 32;
+    // pipeline depth: as deep as shared memory allows while the whole grid
+    // stays resident in one wave (per-block footprint = dynamic smem + the
+    // 1 KB the hardware reserves per block); TMA needs no register budget
+    // for loads, so a few stages per block already keep HBM busy
+    const std::int64_t blocks = std::int64_t(pl.col_tiles) * pl.row_tiles * p.nz;
+    const std::int64_t per_sm = std::max<std::int64_t>(1, ceil_div(blocks, device_sm_count()));
+    const std::int64_t nsteps = ceil_div(ceil_div(p.kg_span, p.kl), p.w);
+    const std::size_t red_tile = std::size_t(p.ml) * p.nl * es;
+    const std::size_t tail = 2 * sizeof(unsigned long long) * 16 + std::size_t(p.nl) * sizeof(std::int64_t);
+    const std::size_t optin = std::size_t(device_smem_optin());
+    auto total = [&](int s) { return 1024 + round_up(std::max(std::size_t(s) * g.stage_bytes, red_tile), 16) + tail; };
+    const int max_stages = int(std::max<std::int64_t>(1, std::min<std::int64_t>(16, nsteps)));
+    int stages = 1;
+    if (const char* e = std::getenv("KTUNE_SIMT_STAGE_BYTES")) {
+        stages = int(std::clamp<std::size_t>(std::size_t(std::strtoull(e, nullptr, 0)) / std::size_t(g.stage_bytes), 1,
+                                             std::size_t(max_stages)));
+    } else {
+        const std::size_t sm_bytes = std::size_t(umma::detail::smem_per_sm());
+        while (stages < max_stages && std::size_t(per_sm) * (total(stages + 1) + 1024) <= sm_bytes) ++stages;
+        if (stages == 1 && max_stages > 1 && std::size_t(per_sm) * (total(1) + 1024) > sm_bytes)
+            stages = std::min(max_stages, 2);  // more than one wave anyway: keep a double buffer
+    }
+    while (stages > 1 && total(stages) > optin) --stages;
+    if (total(stages) > optin) {
+        tl.kernel = nullptr;
+        return tl;
+    }
+    tl.stages = stages;
+    tl.smem = total(stages);
+    return tl;
+}
+
+CUtensorMap tma_map_f32(const void* base, std::int64_t inner, std::int64_t outer, int box_inner, int box_outer, int rb) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
+    cuuint64_t strides[1] = {cuuint64_t(inner) * 4};
+    cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_outer)};
+    cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapSwizzle sw = rb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : rb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                  : rb == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                             : CU_TENSOR_MAP_SWIZZLE_NONE;
+    CUresult r = umma::detail::encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
+                                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    return m;
+}
+
+void launch_gemm_tma(const GemmInput& in, Plan& pl, TmaLaunch& tl, const void* a, const void* b, void* c,
+                     cudaStream_t s) {
+    ktune_dev::GemmProblem<float> prob{static_cast<const float*>(a), static_cast<const float*>(b), in.m, in.n, in.k,
+                                       in.trans_a ? 1 : 0, in.trans_b ? 1 : 0, pl.p.nl};
+    pl.p.out = c;
+    pl.p.stages = tl.stages;
+    const auto& g = tl.g;
+    // A: row-major M x K (K-contiguous boxes {wb, m_l}) or K x M (boxes {m_l, w})
+    CUtensorMap am = pl.arm ? tma_map_f32(a, in.k, in.m, g.a_wb, pl.p.ml, g.a_rb)
+                            : tma_map_f32(a, in.m, in.k, pl.p.ml, pl.p.w, 16);
+    // B: N x K when transposed (boxes {wb, n_l}), else K x N (boxes {n_l, w})
+    CUtensorMap bm = pl.brm ? tma_map_f32(b, in.k, in.n, g.b_wb, pl.p.nl, g.b_rb)
+                            : tma_map_f32(b, in.n, in.k, pl.p.nl, pl.p.w, 16);
+    if (const char* d = std::getenv("KTUNE_SIMT_DEBUG")) pl.p.dbg = reinterpret_cast<long long*>(std::strtoull(d, nullptr, 0));
+    prepare(tl.kernel, tl.smem);
+    ktune_dev::TmaGeom geom = g;
+    void* args[] = {&am, &bm, &prob, &pl.p, &geom};
+    launch(tl.kernel, pl.grid, dim3(unsigned(tl.threads)), args, tl.smem, s, 1, "gemm (tma) launch");
+}
+
 template <typename T>
 void launch_gemm_t(const GemmInput& in, Plan& pl, Mode mode, const void* a, const void* b, void* c, cudaStream_t s) {
     ktune_dev::GemmProblem<T> prob{static_cast<const T*>(a), static_cast<const T*>(b), in.m, in.n, in.k,
@@ -432,7 +589,10 @@ void gemm(const GemmInput& in, const GemmTuning& t, Mode mode, const void* a, co
     }
     Plan pl = gemm_plan(in, t, a, b);
     bind_workspace(pl, ws, ws_bytes);
-    if (in.dtype == Dtype::f32) launch_gemm_t<float>(in, pl, mode, a, b, c, stream);
+    pick(false, in.dtype, mode, pl);  // resolves pl.generic
+    TmaLaunch tl = tma_geometry(in, pl, mode, a, b);
+    if (tl.kernel != nullptr) launch_gemm_tma(in, pl, tl, a, b, c, stream);
+    else if (in.dtype == Dtype::f32) launch_gemm_t<float>(in, pl, mode, a, b, c, stream);
     else launch_gemm_t<double>(in, pl, mode, a, b, c, stream);
 }
 
@@ -452,6 +612,11 @@ LaunchInfo gemm_launch_info(const GemmInput& in, const GemmTuning& t, Mode mode)
     if (is_tensor_core_dtype(in.dtype)) return umma::gemm_launch_info(in, t);
     Plan pl = gemm_plan(in, t);
     pick(false, in.dtype, mode, pl);
+    // nullptr operands: assume cudaMalloc alignment
+    static const float aligned_probe[4] alignas(16) = {};
+    TmaLaunch tl = tma_geometry(in, pl, mode, aligned_probe, aligned_probe);
+    if (tl.kernel != nullptr)
+        return LaunchInfo{tl.threads, tl.smem, int(pl.grid.x), int(pl.grid.y), int(pl.grid.z), false, "simt-tma"};
     return LaunchInfo{pl.threads, pl.smem, int(pl.grid.x), int(pl.grid.y), int(pl.grid.z), pl.generic, "simt"};
 }
 

@@ -61,11 +61,20 @@ struct SimtParams {
     long long* dbg;             // optional timeline probe (KTUNE_SIMT_DEBUG): blocks x = 0, y in {0, 1}
 };
 
+// Timeline probe (debug builds of a measurement: KTUNE_SIMT_DEBUG = device
+// address of a [blocks][8] int64 buffer): thread 0 of every block records
+// %globaltimer at up to 8 points, plus its SM id in slot 7.
 __device__ __forceinline__ void simt_probe(const SimtParams& p, int slot) {
-    if (p.dbg == nullptr || blockIdx.x != 0 || blockIdx.y > 1 || threadIdx.x != 0) return;
+    if (p.dbg == nullptr || threadIdx.x != 0) return;
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.dbg[(blockIdx.y * gridDim.z + blockIdx.z) * 8 + slot] = (long long)t;
+    const std::int64_t b = (std::int64_t(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    p.dbg[b * 8 + slot] = (long long)t;
+    if (slot == 0) {
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        p.dbg[b * 8 + 7] = sm;
+    }
 }
 
 // Per-thread cp.async chunks of one operand, precomputed once per block for
@@ -229,6 +238,90 @@ __device__ __forceinline__ void cp_async_wait_dyn(int n) {
         case 5: cp_async_wait<5>(); break;
         default: cp_async_wait<6>(); break;
     }
+}
+
+// ---- output: direct store, or the k_g merge by the last-arriving slice ----
+// Every slice publishes its partial tile to ws[g] and takes a ticket from the
+// tile's 32-bit arrival counter (one acq_rel atomic add).  The slice that
+// arrives last -- whichever z it has -- folds all partials in slice order,
+// its own from registers (backends.cpp:320-325: c = ((0 + s_0) + s_1) + ...)
+// and resets the counter to zero for the next launch on this workspace.  No
+// block ever waits for another, so nothing depends on the order blocks are
+// dispatched in.  Must be reached by every thread of the block.
+template <typename T, bool PARITY, int TILE, class Prob, class IdxFn>
+__device__ __forceinline__ void simt_store_or_merge(const Prob& prob, const SimtParams& p, const T* blk, int n,
+                                                    bool owner, IdxFn idx_of) {
+    using A = Arith<T, PARITY>;
+    T* out = static_cast<T*>(p.out);
+    if (p.nz == 1) {
+        if (owner)
+#pragma unroll
+            for (int e = 0; e < TILE; ++e) {
+                if (e >= n) break;
+                std::int64_t row, oc;
+                idx_of(e, row, oc);
+                if (row < p.rows && oc >= 0) out[prob.out_index(row, oc)] = A::add(T(0), blk[e]);
+            }
+        return;
+    }
+    T* ws = static_cast<T*>(p.ws);
+    const int g = int(blockIdx.z);
+    const std::int64_t tile_id = std::int64_t(blockIdx.y) * gridDim.x + blockIdx.x;
+    std::int64_t idx[TILE];
+#pragma unroll
+    for (int e = 0; e < TILE; ++e) {
+        idx[e] = -1;
+        if (e < n) {
+            std::int64_t row, oc;
+            idx_of(e, row, oc);
+            if (row < p.rows && oc >= 0) idx[e] = prob.out_index(row, oc);
+        }
+    }
+    if (owner)
+#pragma unroll
+        for (int e = 0; e < TILE; ++e)
+            if (e < n && idx[e] >= 0) __stcg(ws + std::int64_t(g) * p.out_elems + idx[e], blk[e]);
+    __shared__ int s_last;
+    // bar.sync orders every thread's partial stores before thread 0's
+    // gpu-scope release (cumulative); its acquire half orders the folding
+    // slice's loads after every other slice's stores
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned* ctr = reinterpret_cast<unsigned*>(p.flags) + tile_id;
+        unsigned prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;\n" : "=r"(prev) : "l"(ctr) : "memory");
+        const int last = int(prev) + 1 == p.nz;
+        if (last) asm volatile("st.relaxed.gpu.global.u32 [%0], 0;\n" ::"l"(ctr) : "memory");
+        s_last = last;
+    }
+    __syncthreads();
+    if (!s_last || !owner) return;
+    // Batches of FB slices: up to 64 independent L2 loads in flight, then the
+    // adds in slice order (the order is what parity fixes, not the loads).
+    T v[TILE];
+#pragma unroll
+    for (int e = 0; e < TILE; ++e) v[e] = T(0);
+    constexpr int FB = TILE >= 64 ? 1 : 64 / TILE;
+    for (int g0 = 0; g0 < p.nz; g0 += FB) {
+        T part[FB][TILE];
+#pragma unroll
+        for (int f = 0; f < FB; ++f) {
+            const int gg = g0 + f;
+            const T* src = ws + std::int64_t(gg) * p.out_elems;
+#pragma unroll
+            for (int e = 0; e < TILE; ++e)
+                part[f][e] = (gg < p.nz && gg != g && e < n && idx[e] >= 0) ? __ldcg(src + idx[e]) : blk[e];
+        }
+#pragma unroll
+        for (int f = 0; f < FB; ++f)
+            if (g0 + f < p.nz)
+#pragma unroll
+                for (int e = 0; e < TILE; ++e)
+                    if (e < n) v[e] = A::add(v[e], part[f][e]);
+    }
+#pragma unroll
+    for (int e = 0; e < TILE; ++e)
+        if (e < n && idx[e] >= 0) out[idx[e]] = v[e];
 }
 
 // Generic (runtime-tile) kernels keep accumulators in local memory up to this
@@ -684,109 +777,12 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads : LaunchCap<MS_, NS_, 
     }
 
     simt_probe(p, 4);
-    // ---- output: direct store, or k_g partial + last-block ordered merge ---
     const bool owner = (lg == p.kl - 1);
-    T* out = static_cast<T*>(p.out);
-    if (p.nz == 1) {
-        if (owner)
-#pragma unroll
-            for (int i = 0; i < MS; ++i) {
-                const std::int64_t row = row0 + row_of(i);
-                if (row >= p.rows) continue;
-                for (int j = 0; j < NS; ++j) {
-                    const std::int64_t oc = col_out[col_of(j)];
-                    if (oc >= 0) out[prob.out_index(row, oc)] = A::add(T(0), blk[i * NS + j]);
-                }
-            }
-        return;
-    }
-    // Slices 0..nz-2 publish their partial tile and a per-launch token; the
-    // block of the last slice (scheduled after every lower-z block has
-    // started, so the wait cannot deadlock) waits for all tokens and folds
-    // the partials in slice order, its own last (backends.cpp:320-325).
-    // Tokens are unique per launch, so the workspace never needs zeroing.
-    T* ws = static_cast<T*>(p.ws);
-    const std::int64_t tiles = std::int64_t(gridDim.x) * gridDim.y;
-    const std::int64_t tile_id = std::int64_t(rt) * gridDim.x + ct;
-    if (g < p.nz - 1) {
-        if (owner)
-#pragma unroll
-            for (int i = 0; i < MS; ++i) {
-                const std::int64_t row = row0 + row_of(i);
-                if (row >= p.rows) continue;
-#pragma unroll
-                for (int j = 0; j < NS; ++j) {
-                    const std::int64_t oc = col_out[col_of(j)];
-                    if (oc >= 0) __stcg(ws + std::int64_t(g) * p.out_elems + prob.out_index(row, oc), blk[i * NS + j]);
-                }
-            }
-        // bar.sync orders every thread's partial stores before thread 0's
-        // release; a gpu-scope release is cumulative over them (PTX memory
-        // model), so no per-thread fence is needed.
-        __syncthreads();
-        if (tid == 0) {
-            unsigned long long* flag = p.flags + std::int64_t(g) * tiles + tile_id;
-            asm volatile("fence.acq_rel.gpu;\nst.release.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(p.token)
-                         : "memory");
-        }
-        simt_probe(p, 5);
-        return;
-    }
-    for (int gg = tid; gg < p.nz - 1; gg += nthreads) {
-        unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + tile_id;
-        unsigned long long v;
-        while (true) {
-            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(flag) : "memory");
-            if (v == p.token) {
-                // consumed: clear it, so a re-launch with the same token (a
-                // replayed CUDA graph) waits for its own publication
-                asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(0ull) : "memory");
-                break;
-            }
-            __nanosleep(32);
-        }
-    }
-    __syncthreads();
-    simt_probe(p, 6);
-    if (owner) {
-        // Fold the published partials in slice order (backends.cpp:320-325),
-        // own slice last.  All partials of one slice are loaded before any
-        // add, so a slice costs one L2 round trip rather than one per output.
-        std::int64_t idx[TILE];
-        T v[TILE];
-#pragma unroll
-        for (int i = 0; i < MS; ++i)
-#pragma unroll
-            for (int j = 0; j < NS; ++j) {
-                const std::int64_t row = row0 + row_of(i);
-                const std::int64_t oc = col_out[col_of(j)];
-                idx[i * NS + j] = (row < p.rows && oc >= 0) ? prob.out_index(row, oc) : -1;
-                v[i * NS + j] = T(0);
-            }
-        // Batches of FB slices: FB*TILE independent L2 loads in flight, then
-        // the adds in slice order (the order is what parity fixes, not the loads).
-        constexpr int FB = TILE >= 32 ? 1 : 32 / TILE;
-        for (int g0 = 0; g0 < p.nz - 1; g0 += FB) {
-            T part[FB][TILE];
-#pragma unroll
-            for (int f = 0; f < FB; ++f) {
-                const T* src = ws + std::int64_t(g0 + f) * p.out_elems;
-                const bool live = g0 + f < p.nz - 1;
-#pragma unroll
-                for (int e = 0; e < MS * NS; ++e) part[f][e] = (live && idx[e] >= 0) ? __ldcg(src + idx[e]) : T(0);
-            }
-#pragma unroll
-            for (int f = 0; f < FB; ++f)
-                if (g0 + f < p.nz - 1)
-#pragma unroll
-                    for (int e = 0; e < MS * NS; ++e) v[e] = A::add(v[e], part[f][e]);
-        }
-#pragma unroll
-        for (int e = 0; e < MS * NS; ++e)
-            if (idx[e] >= 0) out[idx[e]] = A::add(v[e], blk[e]);
-    }
-    __syncthreads();
-    simt_probe(p, 7);
+    simt_store_or_merge<T, PARITY, TILE>(prob, p, blk, MS * NS, owner, [&](int e, std::int64_t& row, std::int64_t& oc) {
+        const int i = e / NS, j = e - (e / NS) * NS;
+        row = row0 + row_of(i);
+        oc = col_out[col_of(j)];
+    });
 }
 
 }  // namespace ktune_dev

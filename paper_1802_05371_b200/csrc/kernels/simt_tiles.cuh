@@ -59,6 +59,15 @@ KTUNE_DECLARE_GEMM_LOOKUPS(f32, parity_narrow)
 KTUNE_DECLARE_GEMM_LOOKUPS(f32, fast_narrow)
 KTUNE_DECLARE_LOOKUP(conv, f32, parity_narrow)
 KTUNE_DECLARE_LOOKUP(conv, f32, fast_narrow)
+// TMA-fed fp32 GEMM (simt_tma.cuh), NARROW tile list, no generic instantiation
+const void* simt_tma_f32_parity_nn(int ms, int ns, int ks);
+const void* simt_tma_f32_parity_tn(int ms, int ns, int ks);
+const void* simt_tma_f32_parity_nt(int ms, int ns, int ks);
+const void* simt_tma_f32_parity_tt(int ms, int ns, int ks);
+const void* simt_tma_f32_fast_nn(int ms, int ns, int ks);
+const void* simt_tma_f32_fast_tn(int ms, int ns, int ks);
+const void* simt_tma_f32_fast_nt(int ms, int ns, int ks);
+const void* simt_tma_f32_fast_tt(int ms, int ns, int ks);
 
 // Max threads the (ms,ns,ks) instantiation was compiled for.
 inline int simt_thread_cap(int ms, int ns, int ks) {

@@ -633,7 +633,7 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     if (p.nz > 1) {
         pl.flag_bytes = (std::size_t(p.tiles_m) * (pl.pair ? 2 : 1) * p.tiles_n * std::size_t(p.nz - 1) * 8 + 255) /
                         256 * 256;
-        pl.ws_bytes = pl.flag_bytes + std::size_t(p.nz - 1) * std::size_t(in.m) * std::size_t(in.n) * 4;
+        pl.ws_bytes = dev::kSplitCounterBytes + pl.flag_bytes + std::size_t(p.nz - 1) * std::size_t(in.m) * std::size_t(in.n) * 4;
     }
     return pl;
 }
@@ -661,8 +661,9 @@ void gemm(const GemmInput& in, const GemmTuning& t, const void* a, const void* b
         if (ws == nullptr || ws_bytes < pl.ws_bytes)
             throw workspace_error("workspace of " + std::to_string(ws_bytes) + " bytes is smaller than the " +
                                   std::to_string(pl.ws_bytes) + " bytes this tuning needs");
-        p.flags = static_cast<unsigned long long*>(ws);
-        p.ws = reinterpret_cast<float*>(static_cast<unsigned char*>(ws) + pl.flag_bytes);
+        // past the SIMT family's zeroed counter region (kernels.hpp)
+        p.flags = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(ws) + dev::kSplitCounterBytes);
+        p.ws = reinterpret_cast<float*>(static_cast<unsigned char*>(ws) + dev::kSplitCounterBytes + pl.flag_bytes);
         p.token = next_token();
     }
     const int es = p.esize;

@@ -504,7 +504,7 @@ ConvPlan conv_plan(const ConvInput& in, const ConvTuning& t) {
     pl.grid = dim3(unsigned(std::min<std::int64_t>(units, num_sms())), 1, 1);
     if (p.nz > 1) {
         pl.flag_bytes = (std::size_t(tiles_sp) * p.tiles_k * std::size_t(p.nz - 1) * 8 + 255) / 256 * 256;
-        pl.ws_bytes = pl.flag_bytes + std::size_t(p.nz - 1) * std::size_t(in.k_filters) * std::size_t(pqn) * 4;
+        pl.ws_bytes = dev::kSplitCounterBytes + pl.flag_bytes + std::size_t(p.nz - 1) * std::size_t(in.k_filters) * std::size_t(pqn) * 4;
     }
     return pl;
 }
@@ -531,8 +531,9 @@ void conv(const ConvInput& in, const ConvTuning& t, const void* images, const vo
         if (ws == nullptr || ws_bytes < pl.ws_bytes)
             throw workspace_error("workspace of " + std::to_string(ws_bytes) + " bytes is smaller than the " +
                                   std::to_string(pl.ws_bytes) + " bytes this tuning needs");
-        p.flags = static_cast<unsigned long long*>(ws);
-        p.ws = reinterpret_cast<float*>(static_cast<unsigned char*>(ws) + pl.flag_bytes);
+        // past the SIMT family's zeroed counter region (kernels.hpp)
+        p.flags = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(ws) + dev::kSplitCounterBytes);
+        p.ws = reinterpret_cast<float*>(static_cast<unsigned char*>(ws) + dev::kSplitCounterBytes + pl.flag_bytes);
         p.token = next_token();
     }
     // images I[c][h][w][n] -> 3-D map {W*N, H, C}; filters F[c][rs][k] -> 3-D map {K, RS, C}
