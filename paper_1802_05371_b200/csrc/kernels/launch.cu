@@ -459,6 +459,7 @@ TmaLaunch tma_geometry(const GemmInput& in, const Plan& pl, Mode mode, const voi
     g.b_grp = int(round_up(std::size_t(g.b_grp), 1024));
     g.stage_bytes = p.kl * (g.a_grp + g.b_grp);
     g.compute_threads = pl.threads;
+    g.neg_zero = 0x80000000u;
     g.producer_warp = (pl.threads + 31) / 32;
     tl.threads = g.producer_warp * 32 + 32;
     // pipeline depth: as deep as shared memory allows while the whole grid

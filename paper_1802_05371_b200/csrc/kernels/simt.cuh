@@ -296,12 +296,12 @@ __device__ __forceinline__ void simt_store_or_merge(const Prob& prob, const Simt
     }
     __syncthreads();
     if (!s_last || !owner) return;
-    // Batches of FB slices: up to 64 independent L2 loads in flight, then the
+    // Batches of FB slices: up to 16 independent L2 loads in flight, then the
     // adds in slice order (the order is what parity fixes, not the loads).
     T v[TILE];
 #pragma unroll
     for (int e = 0; e < TILE; ++e) v[e] = T(0);
-    constexpr int FB = TILE >= 64 ? 1 : 64 / TILE;
+    constexpr int FB = TILE >= 16 ? 1 : 16 / TILE;
     for (int g0 = 0; g0 < p.nz; g0 += FB) {
         T part[FB][TILE];
 #pragma unroll

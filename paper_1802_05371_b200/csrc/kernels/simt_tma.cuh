@@ -39,6 +39,7 @@ struct TmaGeom {
     int stage_bytes;     // kl * (a_grp + b_grp)
     int compute_threads; // tm*tn*kl
     int producer_warp;   // warp index of the TMA producer
+    unsigned neg_zero;   // 0x80000000 (-0.0f), opaque to ptxas (see mac2)
 };
 
 __device__ __forceinline__ unsigned tma_smem_u32(const void* p) {
@@ -82,6 +83,40 @@ __device__ __forceinline__ float tma_lds32(unsigned addr) {
     asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v) : "r"(addr));
     return v;
 }
+// ---- packed fp32 (FFMA2 / FMUL2 + FADD2, sm_100) -------------------------
+// Two accumulators per 64-bit register pair: one instruction issues two
+// multiply-adds, halving the FMA issue slots of the register tile.  PARITY
+// keeps the separately rounded multiply and add of the reference
+// (backends.cpp:299-306): mul.rn.f32x2 then add.rn.f32x2 round each lane
+// exactly like __fmul_rn / __fadd_rn.  A scalar operand is broadcast to both
+// lanes ({a, a}), which ptxas encodes as the .F32 operand form (no move).
+__device__ __forceinline__ unsigned long long pk2(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float2 up2(unsigned long long v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+// PARITY: the product as fma(a, b, nz) with nz = {-0.0, -0.0} -- exactly
+// round(a*b) for every input (x + -0 == x; -0 keeps the sign of a zero
+// product) -- then add.rn.f32x2.  ptxas contracts a mul.rn.f32x2 /
+// add.rn.f32x2 pair (and an fma with a literal -0) into one FFMA2, which
+// would round once; nz arrives from a kernel parameter, so it cannot.
+template <bool PARITY>
+__device__ __forceinline__ void mac2(unsigned long long& d, unsigned long long a, unsigned long long b,
+                                     unsigned long long nz) {
+    if constexpr (PARITY) {
+        unsigned long long t;
+        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(t) : "l"(a), "l"(b), "l"(nz));
+        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(d) : "l"(t));
+    } else {
+        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+    }
+}
+
 __device__ __forceinline__ void tma_prefetch_map(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(map)) : "memory");
 }
@@ -147,9 +182,16 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 32 : 1024)
     pdl_wait();  // operands / output / workspace may belong to the previous kernel
     simt_probe(p, 1);
 
-    T acc[MS_ * NS_ * KS_];
+    // accumulators: packed pairs along the register tile's columns (NS even),
+    // else along its rows (MS even), else scalar
+    constexpr int PAIR = (NS_ % 2 == 0) ? 1 : ((MS_ % 2 == 0) ? 2 : 0);
+    constexpr int NACC = MS_ * NS_ * KS_;
+    unsigned long long accp[PAIR ? NACC / 2 : 1];
+    T acc[NACC];
 #pragma unroll
-    for (int i = 0; i < MS_ * NS_ * KS_; ++i) acc[i] = T(0);
+    for (int i = 0; i < NACC; ++i) acc[i] = T(0);
+#pragma unroll
+    for (int i = 0; i < (PAIR ? NACC / 2 : 1); ++i) accp[i] = 0ull;
 
     const int per_group = p.tm * p.tn;
     const int lg = tid / per_group;
@@ -164,9 +206,10 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 32 : 1024)
     if (warp == g.producer_warp) {
         // ---- TMA producer (one lane) ------------------------------------
         if (lane == 0) {
+            int slot = 0;
+            unsigned phase = 0;  // parity of the ring pass (stage reuse count & 1)
             for (int st = 0; st < nsteps; ++st) {
-                const int slot = st % p.stages;
-                if (st >= p.stages) tma_mbar_wait(&empty[slot], unsigned((st / p.stages - 1) & 1));
+                if (st >= p.stages) tma_mbar_wait(&empty[slot], phase ^ 1u);
                 unsigned tx_bytes = 0;
                 for (int gx = 0; gx < p.kl; ++gx) {
                     const std::int64_t glo = min(s_hi, s_lo + gx * kl_span);
@@ -190,6 +233,10 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 32 : 1024)
                         if constexpr (BRM) tma_box_2d(gb + b * g.b_box_stride, &b_map, &full[slot], int(kc) + b * g.b_wb, col0);
                         else tma_box_2d(gb, &b_map, &full[slot], col0, int(kc));
                     }
+                }
+                if (++slot == p.stages) {
+                    slot = 0;
+                    phase ^= 1u;
                 }
             }
         }
@@ -215,20 +262,24 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 32 : 1024)
         const unsigned a_kbytes = unsigned(p.ml * ES);  // !ARM: bytes of one reduction row of the A box
         const unsigned b_kbytes = unsigned(p.nl * ES);
         const int a_wmask = g.a_wb - 1, b_wmask = g.b_wb - 1;
+        const unsigned long long nz2 = (static_cast<unsigned long long>(g.neg_zero) << 32) | g.neg_zero;
+        int slot = 0;
+        unsigned phase = 0;
         for (int st = 0; st < nsteps; ++st) {
-            const int slot = st % p.stages;
             const std::int64_t k0 = my_lo + std::int64_t(st) * p.w;
             const int nv = tid < g.compute_threads ? int(max(std::int64_t(0), min(std::int64_t(p.w), my_hi - k0))) : 0;
-            tma_mbar_wait(&full[slot], unsigned((st / p.stages) & 1));
+            tma_mbar_wait(&full[slot], phase);
             if (st == 0) simt_probe(p, 2);
             const unsigned ga = sbase + unsigned(slot * g.stage_bytes + lg * (g.a_grp + g.b_grp));
             const unsigned gb = ga + unsigned(g.a_grp);
-            auto chunk = [&]<bool FULL>(int kk0, int lim) {
+            // ONEBOX: the step's reduction columns fit one 128-byte box row
+            // (compile-time w <= 32), so chunk offsets need no box index
+            auto chunk = [&]<bool FULL, bool ONEBOX>(int kk0, int lim) {
                 T ak[ARM ? MS_ * VK : 1];
                 T bk[BRM ? NS_ * VK : 1];
                 if constexpr (ARM) {
-                    const unsigned base = ga + unsigned((kk0 >> g.a_lwb) * g.a_box_stride);
-                    const unsigned cb = unsigned((kk0 & a_wmask) * ES);
+                    const unsigned base = ONEBOX ? ga : ga + unsigned((kk0 >> g.a_lwb) * g.a_box_stride);
+                    const unsigned cb = unsigned((ONEBOX ? kk0 : (kk0 & a_wmask)) * ES);
 #pragma unroll
                     for (int i = 0; i < MS_; ++i) {
                         const float4 v = tma_lds128(base + a_off[i] + (cb ^ a_xor[i]));
@@ -236,8 +287,8 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 32 : 1024)
                     }
                 }
                 if constexpr (BRM) {
-                    const unsigned base = gb + unsigned((kk0 >> g.b_lwb) * g.b_box_stride);
-                    const unsigned cb = unsigned((kk0 & b_wmask) * ES);
+                    const unsigned base = ONEBOX ? gb : gb + unsigned((kk0 >> g.b_lwb) * g.b_box_stride);
+                    const unsigned cb = unsigned((ONEBOX ? kk0 : (kk0 & b_wmask)) * ES);
 #pragma unroll
                     for (int j = 0; j < NS_; ++j) {
                         const float4 v = tma_lds128(base + b_off[j] + (cb ^ b_xor[j]));
@@ -283,21 +334,57 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 32 : 1024)
                             }
                         }
                         constexpr int set_mask = KS_ - 1;  // KS_ divides VK: set = c % KS
+                        const int set = c & set_mask;
+                        if constexpr (PAIR == 1) {
 #pragma unroll
-                        for (int i = 0; i < MS_; ++i)
+                            for (int j = 0; j < NS_; j += 2) {
+                                const unsigned long long b2 = pk2(bv[j], bv[j + 1]);
 #pragma unroll
-                            for (int j = 0; j < NS_; ++j) {
-                                T& c_ = acc[((c & set_mask) * MS_ + i) * NS_ + j];
-                                c_ = A::mac(c_, av[i], bv[j]);
+                                for (int i = 0; i < MS_; ++i)
+                                    mac2<PARITY>(accp[((set * MS_ + i) * NS_ + j) / 2], pk2(av[i], av[i]), b2, nz2);
                             }
+                        } else if constexpr (PAIR == 2) {
+#pragma unroll
+                            for (int i = 0; i < MS_; i += 2) {
+                                const unsigned long long a2 = pk2(av[i], av[i + 1]);
+#pragma unroll
+                                for (int j = 0; j < NS_; ++j)
+                                    mac2<PARITY>(accp[((set * NS_ + j) * MS_ + i) / 2], a2, pk2(bv[j], bv[j]), nz2);
+                            }
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < MS_; ++i)
+#pragma unroll
+                                for (int j = 0; j < NS_; ++j) {
+                                    T& c_ = acc[(set * MS_ + i) * NS_ + j];
+                                    c_ = A::mac(c_, av[i], bv[j]);
+                                }
+                        }
                     }
                 }
             };
-            const int nfull = nv & ~(VK - 1);
-            for (int kk0 = 0; kk0 < nfull; kk0 += VK) chunk.template operator()<true>(kk0, VK);
-            if (nfull < nv) chunk.template operator()<false>(nfull, nv - nfull);
+            // full steps of the common widths run fully unrolled (compile-time
+            // smem offsets, loads scheduled ahead of the FFMAs); partial steps
+            // and other widths take the runtime loop with a predicated tail
+            auto full_step = [&]<int W>() {
+#pragma unroll
+                for (int kk0 = 0; kk0 < W; kk0 += VK) chunk.template operator()<true, (W * ES <= 128)>(kk0, VK);
+            };
+            if (nv == p.w && p.w == 16) full_step.template operator()<16>();
+            else if (nv == p.w && p.w == 32) full_step.template operator()<32>();
+            else if (nv == p.w && p.w == 8) full_step.template operator()<8>();
+            else if (nv == p.w && p.w == 64) full_step.template operator()<64>();
+            else {
+                const int nfull = nv & ~(VK - 1);
+                for (int kk0 = 0; kk0 < nfull; kk0 += VK) chunk.template operator()<true, false>(kk0, VK);
+                if (nfull < nv) chunk.template operator()<false, false>(nfull, nv - nfull);
+            }
             __syncwarp();
             if (lane == 0) tma_mbar_arrive(&empty[slot]);
+            if (++slot == p.stages) {
+                slot = 0;
+                phase ^= 1u;
+            }
         }
     }
     // every stage consumed (compute warps waited on each "full"), so all TMA
@@ -306,6 +393,25 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 32 : 1024)
     simt_probe(p, 3);
     pdl_launch_dependents();
 
+    if constexpr (PAIR == 1) {
+#pragma unroll
+        for (int q = 0; q < NACC / 2; ++q) {
+            const float2 v = up2(accp[q]);
+            acc[2 * q] = v.x;
+            acc[2 * q + 1] = v.y;
+        }
+    } else if constexpr (PAIR == 2) {  // pairs ordered [set][j][i / 2]
+#pragma unroll
+        for (int st = 0; st < KS_; ++st)
+#pragma unroll
+            for (int j = 0; j < NS_; ++j)
+#pragma unroll
+                for (int i = 0; i < MS_; i += 2) {
+                    const float2 v = up2(accp[((st * NS_ + j) * MS_ + i) / 2]);
+                    acc[(st * MS_ + i) * NS_ + j] = v.x;
+                    acc[(st * MS_ + i + 1) * NS_ + j] = v.y;
+                }
+    }
     // ---- fold: k_s sets within a thread, then k_l groups in order ----------
     T blk[TILE];
     T* red = reinterpret_cast<T*>(stages_mem);
