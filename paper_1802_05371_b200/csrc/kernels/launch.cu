@@ -460,6 +460,7 @@ TmaLaunch tma_geometry(const GemmInput& in, const Plan& pl, Mode mode, const voi
     g.stage_bytes = p.kl * (g.a_grp + g.b_grp);
     g.compute_threads = pl.threads;
     g.neg_zero = 0x80000000u;
+    g.compute_only = std::getenv("KTUNE_SIMT_COMPUTE_ONLY") != nullptr ? 1 : 0;
     g.producer_warp = (pl.threads + 31) / 32;
     tl.threads = g.producer_warp * 32 + 32;
     // pipeline depth: as deep as shared memory allows while the whole grid
@@ -484,7 +485,10 @@ TmaLaunch tma_geometry(const GemmInput& in, const Plan& pl, Mode mode, const voi
         if (stages == 1 && max_stages > 1 && std::size_t(per_sm) * (total(1) + 1024) > sm_bytes)
             stages = std::min(max_stages, 2);  // more than one wave anyway: keep a double buffer
     }
-    while (stages > 1 && total(stages) > optin) --stages;
+    // the consumers wait for step s+1's stage before releasing step s's, so a
+    // multi-step pipeline needs two stages at least
+    if (max_stages >= 2) stages = std::max(stages, 2);
+    while (stages > 2 && total(stages) > optin) --stages;
     if (total(stages) > optin) {
         tl.kernel = nullptr;
         return tl;

@@ -298,6 +298,8 @@ __device__ __forceinline__ void simt_store_or_merge(const Prob& prob, const Simt
     if (!s_last || !owner) return;
     // Batches of FB slices: up to 16 independent L2 loads in flight, then the
     // adds in slice order (the order is what parity fixes, not the loads).
+    // Wider batches were measured slower: the kernel's register count is set
+    // by its peak, and the extra fold registers cost resident blocks.
     T v[TILE];
 #pragma unroll
     for (int e = 0; e < TILE; ++e) v[e] = T(0);

@@ -40,6 +40,7 @@ struct TmaGeom {
     int compute_threads; // tm*tn*kl
     int producer_warp;   // warp index of the TMA producer
     unsigned neg_zero;   // 0x80000000 (-0.0f), opaque to ptxas (see mac2)
+    int compute_only;    // measurement aid (KTUNE_SIMT_COMPUTE_ONLY): no TMA, no stage waits -- wrong results
 };
 
 __device__ __forceinline__ unsigned tma_smem_u32(const void* p) {
@@ -155,10 +156,12 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 32 : 1024)
     const std::int64_t row0 = std::int64_t(rt) * p.ml;
     const int col0 = ct * p.nl;
 
-    const std::int64_t s_lo = min(p.red, std::int64_t(gz) * p.kg_span);
-    const std::int64_t s_hi = min(p.red, s_lo + p.kg_span);
-    const std::int64_t kl_span = (s_hi - s_lo + p.kl - 1) / p.kl;
-    const int nsteps = int((kl_span + p.w - 1) / p.w);
+    // the reduction fits in 31 bits on this path (host-checked): 32-bit ranges
+    const int red_len = int(p.red), kg_span = int(p.kg_span);
+    const int s_lo = min(red_len, gz * kg_span);
+    const int s_hi = min(red_len, s_lo + kg_span);
+    const int kl_span = (s_hi - s_lo + p.kl - 1) / p.kl;
+    const int nsteps = (kl_span + p.w - 1) / p.w;
     const int compute_warps = (g.compute_threads + 31) >> 5;
 
     if (tid == 0) {
@@ -200,29 +203,30 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 32 : 1024)
     const int tx = r_in - ty * p.tn;
     auto row_of = [&](int i) { return ARM ? ty + i * p.tm : ty * MS_ + i; };
     auto col_of = [&](int j) { return BRM ? tx + j * p.tn : tx * NS_ + j; };
-    const std::int64_t my_lo = min(s_hi, s_lo + lg * kl_span);
-    const std::int64_t my_hi = min(s_hi, my_lo + kl_span);
+    const int my_lo = min(s_hi, s_lo + lg * kl_span);
+    const int my_hi = min(s_hi, my_lo + kl_span);
 
-    if (warp == g.producer_warp) {
+    if (warp == g.producer_warp && !g.compute_only) {
         // ---- TMA producer (one lane) ------------------------------------
         if (lane == 0) {
             int slot = 0;
             unsigned phase = 0;  // parity of the ring pass (stage reuse count & 1)
+            const unsigned group_bytes = unsigned(g.a_nbox * g.a_box_bytes + g.b_nbox * g.b_box_bytes);
+            // groups still streaming at step st: those with len(gx) > st*w;
+            // lengths are non-increasing in gx (only the last groups run short)
             for (int st = 0; st < nsteps; ++st) {
                 if (st >= p.stages) tma_mbar_wait(&empty[slot], phase ^ 1u);
-                unsigned tx_bytes = 0;
+                const int off = st * p.w;
+                int live = 0;
                 for (int gx = 0; gx < p.kl; ++gx) {
-                    const std::int64_t glo = min(s_hi, s_lo + gx * kl_span);
-                    const std::int64_t ghi = min(s_hi, glo + kl_span);
-                    if (glo + std::int64_t(st) * p.w < ghi) tx_bytes += unsigned(g.a_nbox * g.a_box_bytes + g.b_nbox * g.b_box_bytes);
+                    const int glo = min(s_hi, s_lo + gx * kl_span);
+                    const int ghi = min(s_hi, glo + kl_span);
+                    live += (glo + off < ghi) ? 1 : 0;
                 }
-                tma_mbar_expect_tx(&full[slot], tx_bytes);
-                unsigned char* stage = stages_mem + std::size_t(slot) * g.stage_bytes;
-                for (int gx = 0; gx < p.kl; ++gx) {
-                    const std::int64_t glo = min(s_hi, s_lo + gx * kl_span);
-                    const std::int64_t ghi = min(s_hi, glo + kl_span);
-                    const std::int64_t kc = glo + std::int64_t(st) * p.w;
-                    if (kc >= ghi) continue;
+                tma_mbar_expect_tx(&full[slot], unsigned(live) * group_bytes);
+                unsigned char* stage = stages_mem + slot * g.stage_bytes;
+                for (int gx = 0; gx < live; ++gx) {
+                    const int kc = min(s_hi, s_lo + gx * kl_span) + off;
                     unsigned char* ga = stage + gx * (g.a_grp + g.b_grp);
                     unsigned char* gb = ga + g.a_grp;
                     for (int b = 0; b < g.a_nbox; ++b) {
@@ -265,21 +269,23 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 32 : 1024)
         const unsigned long long nz2 = (static_cast<unsigned long long>(g.neg_zero) << 32) | g.neg_zero;
         int slot = 0;
         unsigned phase = 0;
+        const int my_len = tid < g.compute_threads ? my_hi - my_lo : 0;
         for (int st = 0; st < nsteps; ++st) {
-            const std::int64_t k0 = my_lo + std::int64_t(st) * p.w;
-            const int nv = tid < g.compute_threads ? int(max(std::int64_t(0), min(std::int64_t(p.w), my_hi - k0))) : 0;
-            tma_mbar_wait(&full[slot], phase);
+            const int nv = max(0, min(p.w, my_len - st * p.w));
+            if (!g.compute_only) tma_mbar_wait(&full[slot], phase);
             if (st == 0) simt_probe(p, 2);
             const unsigned ga = sbase + unsigned(slot * g.stage_bytes + lg * (g.a_grp + g.b_grp));
             const unsigned gb = ga + unsigned(g.a_grp);
-            // ONEBOX: the step's reduction columns fit one 128-byte box row
-            // (compile-time w <= 32), so chunk offsets need no box index
-            auto chunk = [&]<bool FULL, bool ONEBOX>(int kk0, int lim) {
+            // WB > 0: box width known at compile time (full steps; a k-contiguous
+            // box row holds min(w, 128 / ES) columns), so chunk offsets and box
+            // indices fold into constants; WB == 0: runtime widths
+            auto chunk = [&]<bool FULL, int WB>(int kk0, int lim) {
                 T ak[ARM ? MS_ * VK : 1];
                 T bk[BRM ? NS_ * VK : 1];
                 if constexpr (ARM) {
-                    const unsigned base = ONEBOX ? ga : ga + unsigned((kk0 >> g.a_lwb) * g.a_box_stride);
-                    const unsigned cb = unsigned((ONEBOX ? kk0 : (kk0 & a_wmask)) * ES);
+                    const unsigned base = WB ? ga + unsigned(kk0 / (WB ? WB : 1)) * unsigned(g.a_box_stride)
+                                             : ga + unsigned((kk0 >> g.a_lwb) * g.a_box_stride);
+                    const unsigned cb = unsigned((WB ? kk0 % (WB ? WB : 1) : (kk0 & a_wmask)) * ES);
 #pragma unroll
                     for (int i = 0; i < MS_; ++i) {
                         const float4 v = tma_lds128(base + a_off[i] + (cb ^ a_xor[i]));
@@ -287,8 +293,9 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 32 : 1024)
                     }
                 }
                 if constexpr (BRM) {
-                    const unsigned base = ONEBOX ? gb : gb + unsigned((kk0 >> g.b_lwb) * g.b_box_stride);
-                    const unsigned cb = unsigned((ONEBOX ? kk0 : (kk0 & b_wmask)) * ES);
+                    const unsigned base = WB ? gb + unsigned(kk0 / (WB ? WB : 1)) * unsigned(g.b_box_stride)
+                                             : gb + unsigned((kk0 >> g.b_lwb) * g.b_box_stride);
+                    const unsigned cb = unsigned((WB ? kk0 % (WB ? WB : 1) : (kk0 & b_wmask)) * ES);
 #pragma unroll
                     for (int j = 0; j < NS_; ++j) {
                         const float4 v = tma_lds128(base + b_off[j] + (cb ^ b_xor[j]));
@@ -367,8 +374,9 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 32 : 1024)
             // smem offsets, loads scheduled ahead of the FFMAs); partial steps
             // and other widths take the runtime loop with a predicated tail
             auto full_step = [&]<int W>() {
+                constexpr int WB = W * ES <= 128 ? W : 128 / ES;
 #pragma unroll
-                for (int kk0 = 0; kk0 < W; kk0 += VK) chunk.template operator()<true, (W * ES <= 128)>(kk0, VK);
+                for (int kk0 = 0; kk0 < W; kk0 += VK) chunk.template operator()<true, WB>(kk0, VK);
             };
             if (nv == p.w && p.w == 16) full_step.template operator()<16>();
             else if (nv == p.w && p.w == 32) full_step.template operator()<32>();
@@ -376,11 +384,11 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 32 : 1024)
             else if (nv == p.w && p.w == 64) full_step.template operator()<64>();
             else {
                 const int nfull = nv & ~(VK - 1);
-                for (int kk0 = 0; kk0 < nfull; kk0 += VK) chunk.template operator()<true, false>(kk0, VK);
-                if (nfull < nv) chunk.template operator()<false, false>(nfull, nv - nfull);
+                for (int kk0 = 0; kk0 < nfull; kk0 += VK) chunk.template operator()<true, 0>(kk0, VK);
+                if (nfull < nv) chunk.template operator()<false, 0>(nfull, nv - nfull);
             }
             __syncwarp();
-            if (lane == 0) tma_mbar_arrive(&empty[slot]);
+            if (lane == 0 && !g.compute_only) tma_mbar_arrive(&empty[slot]);
             if (++slot == p.stages) {
                 slot = 0;
                 phase ^= 1u;
