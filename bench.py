@@ -345,11 +345,62 @@ def rerank(inp, cands, sets, stream, steps=100, mode="fast"):
     return best
 
 
+def ref_tuning_baseline(ins, tus, hw_json, budget_s=20.0):
+    """The reference CpuBackend::measure (backends.cpp:502-556; warm-up + 3
+    timed executes per sample) on the box's host cores, one sample per
+    thread, over the first samples of the same pre-drawn sequence that a
+    single core finishes in ~1 s (the sequence is heavy-tailed: whole samples
+    up to 1e12 FLOP would take minutes each).  Reported as samples/s of the
+    whole sequence: the measured per-core FLOP rate x cores / (4 executes x
+    the sequence's mean FLOP per sample)."""
+    import ctypes
+    from concurrent.futures import ThreadPoolExecutor
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_libs as O
+    lib = O.reference()
+    if lib is None:
+        return None
+    fn = lib.ref_cpu_measure_gemm
+    fn.argtypes = [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                   ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+    flops = np.array([2.0 * x.m * x.n * x.k for x in ins])
+    cores = os.cpu_count() or 1
+    small = [i for i in range(len(ins)) if flops[i] <= 2.5e9][: cores * 4]
+    hwj = hw_json.encode()
+    done_flops, done = [0.0], [0]
+    t_end = time.perf_counter() + budget_s
+
+    def one(i):
+        if time.perf_counter() > t_end:
+            return
+        x, t = ins[i], tus[i]
+        tv = (ctypes.c_int32 * 8)(t.m_s, t.n_s, t.m_l, t.n_l, t.u, t.k_s, t.k_l, t.k_g)
+        g = ctypes.c_double()
+        if fn(hwj, x.m, x.n, x.k, 1, x.trans_a, x.trans_b, tv, 3, ctypes.byref(g)) == 0:
+            done_flops[0] += 4 * flops[i]
+            done[0] += 1
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(cores) as ex:
+        list(ex.map(one, small))
+    secs = time.perf_counter() - t0
+    if done[0] == 0:
+        return None
+    gflops_host = done_flops[0] / secs / 1e9
+    return {"samples_per_s": gflops_host * 1e9 / (4 * float(flops.mean())), "unit": "samples/s", "cores": cores,
+            "kind": "reference", "measured_samples": done[0], "host_gflops": gflops_host,
+            "sample": f"reference CpuBackend::measure (warm-up + 3 reps) on {done[0]} of the first sequence samples "
+                      f"<= 2.5 GFLOP, {cores} threads, {secs:.1f}s; samples/s = host FLOP rate / (4 x mean "
+                      f"sequence FLOP {flops.mean():.3g})"}
+
+
 def tuning_loop(args, ws, rank, dev):
     """BASELINE configs[4] (bounded): the README tuning pipeline on the B200
-    descriptor -- calibrated sampler, tuning samples pre-drawn and LPT-sharded
-    over the ranks, measured on each GPU, one NCCL all-gather of {index,
-    gflops} records; then (rank 0) the GPU MLP fit and the runtime pick."""
+    descriptor -- calibrated sampler, a fixed pre-drawn sequence of
+    `--tuning-samples` samples LPT-sharded over the ranks (strong scaling:
+    the total is fixed), each rank measuring its share inside the library
+    (batched device timing, resumable checkpoint), one NCCL all-gather of
+    {index, gflops} records; then (rank 0) the GPU MLP fit and runtime pick."""
     import torch
     import torch.distributed as dist
 
@@ -361,7 +412,7 @@ def tuning_loop(args, ws, rank, dev):
     dist_ = P.GemmInputDistribution(shapes=P.gemm_shapes_from_table(os.path.join(K.FIXTURES, "shapes",
                                                                                  "benchmarks.json")),
                                     fixed_fraction=0.25)
-    n = args.tuning_samples * ws
+    n = args.tuning_samples
     K.measure(K.GemmInput(256, 256, 256), K.GemmTuning(2, 2, 32, 32, 8, 1, 1, 1), hw)  # load modules, buffers
     if ws > 1:
         dist.barrier()
@@ -369,22 +420,29 @@ def tuning_loop(args, ws, rank, dev):
     t0 = time.perf_counter()
     csv, stats = P.generate_sharded(sampler, dist_, hw, bounds, n, 42, backend="b200", device=dev)
     torch.cuda.synchronize(dev)
-    el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    el = torch.tensor([time.perf_counter() - t0, stats["measure_s"]], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(el, op=dist.ReduceOp.MAX)
-    secs = float(el.item())
-    out = {"samples": n, "samples_per_s": n / secs, "seconds": secs, "per_gpu_samples": args.tuning_samples,
-           "scaling": "weak", "predraw_s": stats["predraw_s"],
+    secs = float(el[0].item())
+    out = {"samples": n, "samples_per_s": n / secs, "seconds": secs, "n_gpus": ws,
+           "scaling": "strong (fixed pre-drawn sequence, LPT-sharded by 2MNK)",
+           "unlaunchable_redrawn": stats["unlaunchable"], "local_samples": stats["local_samples"],
            "gather": "NCCL all_gather_into_tensor of {index, gflops} records" if ws > 1 else "single rank",
            "pipeline": "README walkthrough on fixtures/hw/b200.json + bounds/gemm_b200.json, seed 42, "
-                       "fixture shapes at 0.25, f32 (reference: generate_gemm_dataset, pipeline.cpp:463-509)",
-           "timing": "host wall clock of the sharded measurement loop, max over ranks",
-           "reference_cpu_samples_per_s_per_core": 0.0068}
+                       "fixture shapes at 0.25, f32 (reference: generate_gemm_dataset, pipeline.cpp:463-509); "
+                       "measurement = CpuBackend protocol on the GPU (warm-up + best of 3, L2 flushed)",
+           "timing": "host wall clock of pre-draw + sharded measurement + gather, max over ranks"}
     if rank == 0:
+        ins, tus, _, _ = P.predraw(sampler, dist_, hw, bounds, n, 42)
+        ref = ref_tuning_baseline(P.as_inputs(ins), P.as_tunings(tus),
+                                  open(os.path.join(K.FIXTURES, "hw", "b200.json")).read())
+        out["cpu_baseline"] = ref
+        if ref:
+            out["ratio_vs_reference_host"] = out["samples_per_s"] / ref["samples_per_s"]
         t1 = time.perf_counter()
         fit = P.train_mlp(csv, epochs=60, seed=7)
         out["mlp_fit"] = {"rows": n, "epochs": 60, "seconds": time.perf_counter() - t1,
-                          "best_val_mse": fit.best_val_mse, "where": "GPU (K7, one CTA)"}
+                          "best_val_mse": fit.best_val_mse}
         inp = K.GemmInput(2560, 32, 2560, "f32")
         space = K.enumerate_legal(inp, hw, bounds)
         P.mlp_predict(fit.model_json, inp, space[:1000])
@@ -402,6 +460,64 @@ def tuning_loop(args, ws, rank, dev):
                                "cold_pick_ms": cold * 1e3, "cold_source": src, "warm_pick_us": warm * 1e6,
                                "warm_source": src2, "top_k": 20, "chosen": pick.values()}
     return out
+
+
+def ref_lib():
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_libs as O
+    return O.reference()
+
+
+def cpu_gemm_tflops(m, n, k, ta, tb, tuple_, rows=None, reps=1):
+    """The reference execute_gemm<float> (backends.cpp:228-329) on every host
+    core (one copy per thread, oracle/_ref); `rows` < m times a row slice of
+    the same GEMM (the executor's cost is linear in M) -- labelled."""
+    import ctypes
+    lib = ref_lib()
+    if lib is None:
+        return None
+    threads = os.cpu_count() or 1
+    mm = rows or m
+    tv = (ctypes.c_int32 * 8)(*tuple_)
+    g, sec = ctypes.c_double(), ctypes.c_double()
+    if lib.ref_host_gemm_gflops(ctypes.c_int64(mm), ctypes.c_int64(n), ctypes.c_int64(k), int(ta), int(tb), tv, reps,
+                                threads, ctypes.byref(g), ctypes.byref(sec)) != 0:
+        return {"error": lib.ref_last_error().decode()[:120]}
+    return {"tflops": g.value / 1e3, "cores": threads, "kind": "reference", "dtype": "f32",
+            "sample": f"{threads} threads x {reps} execute_gemm<float> of {mm}x{n}x{k}" +
+                      (f" (a {mm}-row slice of M={m}: per-FLOP rate)" if rows else "") + f", tuple {list(tuple_)}"}
+
+
+def cpu_conv_tflops(d, tuple_):
+    """The reference CpuBackend::measure(ConvInput) (execute_conv<float>,
+    backends.cpp:331-444; warm-up + 1 timed run) on every host core, one
+    concurrent copy per thread; aggregate FLOP rate."""
+    import ctypes
+    from concurrent.futures import ThreadPoolExecutor
+    lib = ref_lib()
+    if lib is None:
+        return None
+    fn = lib.ref_cpu_measure_conv
+    fn.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_int, ctypes.POINTER(ctypes.c_int32),
+                   ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+    threads = os.cpu_count() or 1
+    hwj = open(os.path.join(ROOT, "paper_1802_05371_b200", "fixtures", "hw", "b200.json")).read().encode()
+    dims = (ctypes.c_int64 * 7)(*d)
+    tv = (ctypes.c_int32 * 12)(*tuple_)
+    rates = []
+
+    def one(_):
+        g = ctypes.c_double()
+        if fn(hwj, dims, 1, tv, 1, ctypes.byref(g)) == 0:
+            rates.append(g.value)
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(one, range(threads)))
+    if not rates:
+        return {"error": lib.ref_last_error().decode()[:120]}
+    return {"tflops": sum(rates) / 1e3, "cores": threads, "kind": "reference", "dtype": "f32",
+            "sample": f"{threads} concurrent CpuBackend::measure (warm-up + 1 run) of the f32 convolution, "
+                      f"tuple {list(tuple_)}"}
 
 
 def other_configs(stream, dev):
@@ -442,7 +558,9 @@ def other_configs(stream, dev):
                      ("T" if inp.trans_b else "N"), "tflops": tf, "us": ms * 1e3, "pick": t.values(),
                      "family": family, "screened": sel.screened, "roofline": roof,
                      "cublas_tflops": inp.flops / cub / 1e9, "ratio_vs_cublas": cub / ms,
-                     "rotating_sets": len(sets)}
+                     "rotating_sets": len(sets),
+                     "cpu_baseline": cpu_gemm_tflops(inp.m, inp.n, inp.k, inp.trans_a, inp.trans_b,
+                                                     (2, 4, 32, 32, 8, 1, 4, 32) if inp.k > 10000 else PAPER_TUPLE)}
         del sets
         torch.cuda.empty_cache()
 
@@ -481,7 +599,8 @@ def other_configs(stream, dev):
             "roofline": {"bound": "tensor", "peak_tflops": peak, "frac": tf / peak,
                          "peak_source": pk["source"] + (" cuBLAS bf16 burst" if dt == "bf16" else
                                                         " bf16 burst / 2 (tf32 rate)")},
-            "cublas_tflops": inp.flops / cub / 1e9, "ratio_vs_cublas": cub / ms}
+            "cublas_tflops": inp.flops / cub / 1e9, "ratio_vs_cublas": cub / ms,
+            "cpu_baseline": cpu_gemm_tflops(n, n, n, ta, tb, (4, 4, 64, 64, 8, 1, 1, 1), rows=32)}
         del sets, A, B
         torch.cuda.empty_cache()
 
@@ -516,6 +635,10 @@ def other_configs(stream, dev):
         xs = [x[0].view(cin.c, cin.h(), cin.w(), cin.n_batch).permute(3, 0, 1, 2).contiguous() for x in sets]
         w = sets[0][1].view(cin.c, cin.r, cin.s, cin.k_filters).permute(3, 0, 1, 2).contiguous()
         cud = time_torch(lambda i: torch.nn.functional.conv2d(xs[i], w), n_sets, stream)
+        # and in channels_last (NHWC, cuDNN's preferred tensor-core layout)
+        xs_cl = [x.contiguous(memory_format=torch.channels_last) for x in xs]
+        w_cl = w.contiguous(memory_format=torch.channels_last)
+        cud_cl = time_torch(lambda i: torch.nn.functional.conv2d(xs_cl[i], w_cl), n_sets, stream)
         tf = cin.flops / ms / 1e9
         byt = (ni + nf) * es + no * 4
         peak_tf = pk["bf16_tflops"] if cin.dtype == "bf16" else 74.4
@@ -527,8 +650,12 @@ def other_configs(stream, dev):
         res[name] = {"shape": [cin.n_batch, cin.p, cin.q, cin.k_filters, cin.c, cin.r, cin.s], "dtype": cin.dtype,
                      "tflops": tf, "us": ms * 1e3, "pick": t.values(), "family": family, "roofline": roof,
                      "layout": "CHWN/CRSK/KPQN (reference layouts, valid mode)",
-                     "cudnn_tflops_nchw": cin.flops / cud / 1e9, "ratio_vs_cudnn": cud / ms, "rotating_sets": n_sets}
-        del sets, xs
+                     "cudnn_tflops_nchw": cin.flops / cud / 1e9, "cudnn_tflops_nhwc": cin.flops / cud_cl / 1e9,
+                     "ratio_vs_cudnn": min(cud, cud_cl) / ms, "rotating_sets": n_sets}
+        if name in ("conv_resnet56_bf16", "conv_resnet56_f32"):
+            res[name]["cpu_baseline"] = cpu_conv_tflops([cin.n_batch, cin.p, cin.q, cin.k_filters, cin.c, cin.r,
+                                                         cin.s], (1, 1, 1, 2, 16, 2, 2, 8, 8, 1, 1, 1))
+        del sets, xs, xs_cl
         torch.cuda.empty_cache()
 
     conv_case("conv_resnet56_bf16", K.ConvInput(16, 56, 56, 64, 64, 3, 3, "bf16"), conv_tc_bounds, tc_conv_key,
@@ -555,7 +682,38 @@ def other_configs(stream, dev):
     B = [x[1].view(512, 512) for x in sets]
     cub = time_torch(lambda i: torch.matmul(A[i], B[i]), len(sets), stream)
     res["sgemm512_fixed_fast"]["cublas_tflops"] = inp.flops / cub / 1e9
+    res["sgemm512_fixed_fast"]["ratio_vs_cublas"] = res["sgemm512_fixed_fast"]["tflops"] / (inp.flops / cub / 1e9)
+    for mode in ("fast", "parity"):
+        tf = res[f"sgemm512_fixed_{mode}"]["tflops"]
+        res[f"sgemm512_fixed_{mode}"]["roofline"] = {"bound": "ffma", "achieved_tflops": tf, "peak_tflops": 74.4,
+                                                     "frac": tf / 74.4}
+    res["sgemm512_fixed_fast"]["cpu_baseline"] = cpu_gemm_tflops(512, 512, 512, 0, 0, (2, 8, 32, 32, 8, 1, 1, 1),
+                                                                 reps=2)
     return res
+
+
+def compact(res):
+    """One short entry per config for the JSON line (the full record goes to
+    stderr and bench_details.json)."""
+    out = {}
+    for k, v in (res or {}).items():
+        if "error" in v:
+            out[k] = {"error": v["error"][:80]}
+            continue
+        e = {"tflops": round(v.get("tflops", 0), 2)}
+        if "roofline" in v:
+            e["frac"] = round(v["roofline"]["frac"], 3)
+            e["bound"] = v["roofline"]["bound"]
+        for ctx in ("ratio_vs_cublas", "ratio_vs_cudnn"):
+            if ctx in v:
+                e[ctx.replace("ratio_", "")] = round(v[ctx], 2)
+        cb = v.get("cpu_baseline")
+        if isinstance(cb, dict) and "tflops" in cb:
+            e["cpu_tflops"] = round(cb["tflops"], 4)
+        if "pick" in v:
+            e["pick"] = v["pick"]
+        out[k] = e
+    return out
 
 
 def our_arm(args):
@@ -570,6 +728,10 @@ def our_arm(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
+        # NCCL's init lines (transport: NVLink / NVLS) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
     w = WORKLOAD
     inp = K.GemmInput(w["m"], w["n"], w["k"], w["dtype"], w["trans_a"], w["trans_b"])
@@ -722,6 +884,31 @@ def our_arm(args):
         "tuning": tuning,
         "other_configs": None if args.no_extras else other_configs(stream, dev),
     }
+    # the full record on stderr and in bench_details.json; stdout carries one
+    # compact JSON line (every config's TFLOP/s, roofline fraction, context
+    # ratio and CPU baseline, within the driver's captured tail)
+    print(json.dumps(line), file=sys.stderr)
+    try:
+        with open(os.path.join(ROOT, "bench_details.json"), "w") as fh:
+            json.dump(line, fh, indent=1)
+    except OSError:
+        pass
+    line["other_configs"] = compact(line["other_configs"])
+    if tuning:
+        t = dict(tuning)
+        rp = t.pop("runtime_pick", None) or {}
+        cb = t.pop("cpu_baseline", None) or {}
+        line["tuning"] = {k: t[k] for k in ("samples", "samples_per_s", "n_gpus", "seconds", "unlaunchable_redrawn",
+                                            "ratio_vs_reference_host") if k in t}
+        line["tuning"]["scaling"] = "strong"
+        line["tuning"]["cpu_samples_per_s"] = cb.get("samples_per_s")
+        line["tuning"]["cpu_cores"] = cb.get("cores")
+        if "mlp_fit" in t:
+            line["tuning"]["mlp_fit_s"] = round(t["mlp_fit"]["seconds"], 3)
+        if rp:
+            line["tuning"]["sweep_pred_per_s"] = round(rp["sweep_predictions_per_s"])
+            line["tuning"]["warm_pick_us"] = round(rp["warm_pick_us"], 1)
+    line["correctness"] = {k: v for k, v in res.items() if k != "cold_single_launch_us"}
     print(json.dumps(line))
     if ws > 1:
         dist.destroy_process_group()
@@ -737,8 +924,22 @@ def main():
     ap.add_argument("--candidates", type=int, default=3000)
     ap.add_argument("--pick", default="", help="fixed tuple m_s,n_s,m_l,n_l,u,k_s,k_l,k_g (skips selection)")
     ap.add_argument("--no-extras", action="store_true", help="headline only (no tuning loop / other configs)")
-    ap.add_argument("--tuning-samples", type=int, default=200, help="tuning-loop samples per GPU (weak scaling)")
+    ap.add_argument("--tuning-samples", type=int, default=10000,
+                    help="tuning-loop samples in total (fixed pre-drawn sequence, sharded over the GPUs)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun (the
+        # driver's own form), rendezvous on 127.0.0.1
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={ws}; using WORLD_SIZE", file=sys.stderr)
     if args.impl == "reference":
         return reference_arm(args)
     return our_arm(args)

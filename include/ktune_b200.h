@@ -249,6 +249,34 @@ KTUNE_API int ktune_predraw_conv(const ktune_hw* hw, const char* bounds_json, co
                                  const ktune_conv_distribution* dist, int32_t n_samples, uint64_t seed,
                                  ktune_conv_input* inputs_out, ktune_conv_tuning* tunings_out, int64_t* attempts,
                                  int64_t* duplicates);
+/* One rank's share of generate_gemm_dataset on the B200 backend (SURVEY
+ * 8(e); reference loop pipeline.cpp:463-509).  Pre-draws the whole sequence
+ * (legal draws this build cannot launch are redrawn and counted in
+ * *unlaunchable), assigns indices to `world` ranks longest-processing-time
+ * first by 2MNK (ktune_shard_lpt), and measures this rank's indices in
+ * batches with one host sync per batch.  checkpoint_path (NULL = none):
+ * every finished batch is appended; a rerun with the same arguments skips
+ * the indices already recorded there.  Outputs: the full sequence
+ * (inputs_out / tunings_out, n_samples entries each, may be NULL) and this
+ * rank's records {index_out[i], gflops_out[i]} (cap entries; *count
+ * written; gflops < 0 = launch failed).  The caller all-gathers the records
+ * and rebuilds the CSV with ktune_gemm_dataset_csv. */
+KTUNE_API int ktune_generate_gemm_shard(const ktune_hw* hw, const char* bounds_json, const char* sampler_json,
+                                        const ktune_gemm_distribution* dist, int32_t n_samples, uint64_t seed,
+                                        int32_t rank, int32_t world, const ktune_measure_options* opts,
+                                        const char* checkpoint_path, ktune_gemm_input* inputs_out,
+                                        ktune_gemm_tuning* tunings_out, int64_t* index_out, double* gflops_out,
+                                        int64_t cap, int64_t* count, int64_t* attempts, int64_t* duplicates,
+                                        int64_t* unlaunchable);
+KTUNE_API int ktune_generate_conv_shard(const ktune_hw* hw, const char* bounds_json, const char* sampler_json,
+                                        const ktune_conv_distribution* dist, int32_t n_samples, uint64_t seed,
+                                        int32_t rank, int32_t world, const ktune_measure_options* opts,
+                                        const char* checkpoint_path, ktune_conv_input* inputs_out,
+                                        ktune_conv_tuning* tunings_out, int64_t* index_out, double* gflops_out,
+                                        int64_t cap, int64_t* count, int64_t* attempts, int64_t* duplicates,
+                                        int64_t* unlaunchable);
+/* LPT assignment of n sample costs to `world` ranks: rank_out[i] = owner. */
+KTUNE_API int ktune_shard_lpt(const double* costs, int64_t n, int32_t world, int32_t* rank_out);
 /* Sequential generation with a backend (0 analytical, 1 b200, 2 b200-parity);
  * CSV text (pipeline.hpp:53-57 header) via ktune_last_text(). */
 KTUNE_API int ktune_generate_gemm(const ktune_hw* hw, const char* bounds_json, const char* sampler_json,

@@ -127,6 +127,19 @@ _SIGNATURES = {
     "ktune_encode_features_gemm": ([_P(GemmInputC), _P(GemmTuningC), _vp], ctypes.c_int),
     "ktune_encode_features_conv": ([_P(ConvInputC), _P(ConvTuningC), _vp], ctypes.c_int),
     "ktune_build_indirection_table": ([_P(ConvInputC), _vp, _i64, _P(_i64)], ctypes.c_int),
+    "ktune_generate_gemm_shard": ([_P(HwC), ctypes.c_char_p, ctypes.c_char_p, _P(GemmDistC), ctypes.c_int32,
+                                   ctypes.c_uint64, ctypes.c_int32, ctypes.c_int32, _P(MeasureOptionsC),
+                                   ctypes.c_char_p,
+                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_int64, _P(ctypes.c_int64), _P(ctypes.c_int64), _P(ctypes.c_int64),
+                                   _P(ctypes.c_int64)], ctypes.c_int),
+    "ktune_generate_conv_shard": ([_P(HwC), ctypes.c_char_p, ctypes.c_char_p, _P(ConvDistC), ctypes.c_int32,
+                                   ctypes.c_uint64, ctypes.c_int32, ctypes.c_int32, _P(MeasureOptionsC),
+                                   ctypes.c_char_p,
+                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_int64, _P(ctypes.c_int64), _P(ctypes.c_int64), _P(ctypes.c_int64),
+                                   _P(ctypes.c_int64)], ctypes.c_int),
+    "ktune_shard_lpt": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p], ctypes.c_int),
     "ktune_gemm_workspace_size": ([_P(GemmInputC), _P(GemmTuningC), _P(ctypes.c_size_t)], ctypes.c_int),
     "ktune_gemm_launch_info": ([_P(GemmInputC), _P(GemmTuningC), ctypes.c_int, _P(ctypes.c_int), _P(ctypes.c_size_t),
                                 _P(ctypes.c_int), ctypes.c_char_p, ctypes.c_size_t], ctypes.c_int),

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <functional>
 #include <limits>
 #include <map>
 #include <memory>
@@ -52,6 +53,7 @@ struct DeviceState {
     cudaEvent_t ev0{nullptr}, ev1{nullptr};
     Operand ops[2];
     DevBuf out, ws;
+    std::vector<cudaEvent_t> pool;  // timing events of measure_*_many
     // host-buffer staging
     DevBuf ha, hb, hc, hws;
     void init() {
@@ -154,6 +156,110 @@ MeasureResult measure_conv_device(const HardwareDescriptor& hw, const ConvInput&
     return time_it(st, opt, flops, [&] {
         dev::conv(in, t, opt.mode, img, flt, st.out.ptr, st.ws.ptr, st.ws.bytes, st.stream);
     });
+}
+
+namespace {
+
+template <typename In, typename Tu, typename Setup>
+std::vector<double> time_many(const std::vector<In>& ins, const std::vector<Tu>& tus, const MeasureOptions& opt,
+                              Setup setup) {
+    if (ins.size() != tus.size()) throw std::invalid_argument("measure_many: inputs / tunings size mismatch");
+    if (opt.repetitions < 1) throw std::invalid_argument("measure: repetitions must be >= 1");
+    DeviceState& st = state();
+    std::lock_guard<std::mutex> lock(st.mu);
+    st.init();
+    const std::size_t n = ins.size();
+    const std::size_t need = n * std::size_t(opt.repetitions) * 2;
+    while (st.pool.size() < need) {
+        cudaEvent_t e;
+        check(cudaEventCreate(&e), "cudaEventCreate");
+        st.pool.push_back(e);
+    }
+    std::vector<double> out(n, -1.0), flops(n, 0.0);
+    std::vector<char> ok(n, 0);
+    for (std::size_t i = 0; i < n; ++i) {
+        std::function<void()> launch;
+        try {
+            launch = setup(st, ins[i], tus[i], flops[i]);  // legality, operands, workspace, plan
+            for (int w = 0; w < std::max(0, opt.warmup); ++w) launch();
+        } catch (const unsupported_error&) {
+            continue;  // outside this build's envelope: reported as -1
+        }
+        for (int r = 0; r < opt.repetitions; ++r) {
+            if (opt.flush_l2) dev::l2_flush(st.stream);
+            check(cudaEventRecord(st.pool[(i * opt.repetitions + r) * 2], st.stream), "cudaEventRecord");
+            launch();
+            check(cudaEventRecord(st.pool[(i * opt.repetitions + r) * 2 + 1], st.stream), "cudaEventRecord");
+        }
+        ok[i] = 1;
+    }
+    check(cudaStreamSynchronize(st.stream), "cudaStreamSynchronize");
+    for (std::size_t i = 0; i < n; ++i) {
+        if (!ok[i]) continue;
+        double best = std::numeric_limits<double>::infinity();
+        for (int r = 0; r < opt.repetitions; ++r) {
+            float ms = 0;
+            check(cudaEventElapsedTime(&ms, st.pool[(i * opt.repetitions + r) * 2],
+                                       st.pool[(i * opt.repetitions + r) * 2 + 1]),
+                  "cudaEventElapsedTime");
+            best = std::min(best, std::max(double(ms) * 1e-3, 1e-9));
+        }
+        out[i] = flops[i] / best / 1e9;
+    }
+    return out;
+}
+
+}  // namespace
+
+std::vector<double> measure_gemm_many(const HardwareDescriptor& hw, const std::vector<GemmInput>& in,
+                                      const std::vector<GemmTuning>& t, const MeasureOptions& opt) {
+    return time_many(in, t, opt, [&](DeviceState& st, const GemmInput& x, const GemmTuning& tu, double& flops) {
+        require_legal(is_legal(x, tu, hw));
+        (void)dev::gemm_launch_info(x, tu, opt.mode);  // throws unsupported_error before any launch
+        const void* a = operand(st, 0, x.dtype, x.m * x.k, opt.seed);
+        const void* b = operand(st, 1, x.dtype, x.k * x.n, opt.seed);
+        st.out.reserve(std::size_t(x.m * x.n) * output_elem_size(x.dtype), false);
+        st.ws.reserve(dev::gemm_workspace_bytes(x, tu), true);
+        flops = 2.0 * double(x.m) * double(x.n) * double(x.k);
+        return std::function<void()>([&st, x, tu, a, b, mode = opt.mode] {
+            dev::gemm(x, tu, mode, a, b, st.out.ptr, st.ws.ptr, st.ws.bytes, st.stream);
+        });
+    });
+}
+
+std::vector<double> measure_conv_many(const HardwareDescriptor& hw, const std::vector<ConvInput>& in,
+                                      const std::vector<ConvTuning>& t, const MeasureOptions& opt) {
+    return time_many(in, t, opt, [&](DeviceState& st, const ConvInput& x, const ConvTuning& tu, double& flops) {
+        require_legal(is_legal(x, tu, hw));
+        (void)dev::conv_launch_info(x, tu, opt.mode);
+        const void* img = operand(st, 0, x.dtype, x.c * x.h() * x.w() * x.n_batch, opt.seed);
+        const void* flt = operand(st, 1, x.dtype, x.c * x.r * x.s * x.k_filters, opt.seed);
+        st.out.reserve(std::size_t(x.k_filters * x.p * x.q * x.n_batch) * output_elem_size(x.dtype), false);
+        st.ws.reserve(dev::conv_workspace_bytes(x, tu), true);
+        flops = 2.0 * double(x.n_batch) * double(x.p) * double(x.q) * double(x.k_filters) * double(x.c) *
+                double(x.r) * double(x.s);
+        return std::function<void()>([&st, x, tu, img, flt, mode = opt.mode] {
+            dev::conv(x, tu, mode, img, flt, st.out.ptr, st.ws.ptr, st.ws.bytes, st.stream);
+        });
+    });
+}
+
+bool B200Backend::accepts(const GemmInput& in, const GemmTuning& t) const {
+    try {
+        (void)dev::gemm_launch_info(in, t, opt_.mode);
+        return true;
+    } catch (const unsupported_error&) {
+        return false;
+    }
+}
+
+bool B200Backend::accepts(const ConvInput& in, const ConvTuning& t) const {
+    try {
+        (void)dev::conv_launch_info(in, t, opt_.mode);
+        return true;
+    } catch (const unsupported_error&) {
+        return false;
+    }
 }
 
 B200Backend::B200Backend(HardwareDescriptor hw, MeasureOptions opt) : hw_(std::move(hw)), opt_(opt) {

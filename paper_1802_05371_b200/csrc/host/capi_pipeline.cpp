@@ -110,6 +110,27 @@ std::unique_ptr<PerfPredictor> make_predictor(const char* model_json, const Hard
 std::mutex g_select_mu;
 std::map<std::string, GemmTuning> g_select_memo;
 
+template <typename In, typename Tu, typename Draw, typename OutIn, typename OutTu>
+void shard_out(const std::vector<Draw>& draws, const std::vector<ShardRecord>& recs, const GenerateReport& rep,
+               In* inputs_out, Tu* tunings_out, int64_t* index_out, double* gflops_out, int64_t cap, int64_t* count,
+               int64_t* attempts, int64_t* duplicates, int64_t* unlaunchable, OutIn out_in_, OutTu out_t_) {
+    if (inputs_out)
+        for (std::size_t i = 0; i < draws.size(); ++i) inputs_out[i] = out_in_(draws[i].input);
+    if (tunings_out)
+        for (std::size_t i = 0; i < draws.size(); ++i) tunings_out[i] = out_t_(draws[i].tuning);
+    if (int64_t(recs.size()) > cap)
+        throw std::invalid_argument("shard: " + std::to_string(recs.size()) + " records exceed cap " +
+                                    std::to_string(cap));
+    for (std::size_t i = 0; i < recs.size(); ++i) {
+        index_out[i] = recs[i].index;
+        gflops_out[i] = recs[i].gflops;
+    }
+    *count = int64_t(recs.size());
+    if (attempts) *attempts = rep.attempts;
+    if (duplicates) *duplicates = rep.duplicates_rejected;
+    if (unlaunchable) *unlaunchable = rep.unlaunchable_rejected;
+}
+
 }  // namespace
 
 extern "C" {
@@ -191,6 +212,60 @@ int ktune_predraw_gemm(const ktune_hw* hw, const char* bounds_json, const char* 
         }
         if (attempts) *attempts = rep.attempts;
         if (duplicates) *duplicates = rep.duplicates_rejected;
+    });
+}
+
+int ktune_generate_gemm_shard(const ktune_hw* hw, const char* bounds_json, const char* sampler_json,
+                              const ktune_gemm_distribution* dist, int32_t n_samples, uint64_t seed, int32_t rank,
+                              int32_t world, const ktune_measure_options* opts, const char* checkpoint_path,
+                              ktune_gemm_input* inputs_out, ktune_gemm_tuning* tunings_out, int64_t* index_out,
+                              double* gflops_out, int64_t cap, int64_t* count, int64_t* attempts,
+                              int64_t* duplicates, int64_t* unlaunchable) {
+    return guard([&] {
+        need(sampler_json, "sampler_json");
+        need(index_out, "index_out");
+        need(gflops_out, "gflops_out");
+        need(count, "count");
+        GenerateReport rep;
+        std::vector<GemmDraw> draws;
+        auto recs = generate_gemm_shard(CategoricalModel::from_json_text(sampler_json), gemm_dist(dist),
+                                        gemm_bounds(bounds_json), conv_hw(hw), n_samples, seed, rank, world,
+                                        opts_of(opts), checkpoint_path ? checkpoint_path : "", &draws, &rep);
+        shard_out(draws, recs, rep, inputs_out, tunings_out, index_out, gflops_out, cap, count, attempts, duplicates,
+                  unlaunchable, [](const GemmInput& x) { return out_in(x); },
+                  [](const GemmTuning& x) { return out_t(x); });
+    });
+}
+
+int ktune_generate_conv_shard(const ktune_hw* hw, const char* bounds_json, const char* sampler_json,
+                              const ktune_conv_distribution* dist, int32_t n_samples, uint64_t seed, int32_t rank,
+                              int32_t world, const ktune_measure_options* opts, const char* checkpoint_path,
+                              ktune_conv_input* inputs_out, ktune_conv_tuning* tunings_out, int64_t* index_out,
+                              double* gflops_out, int64_t cap, int64_t* count, int64_t* attempts,
+                              int64_t* duplicates, int64_t* unlaunchable) {
+    return guard([&] {
+        need(sampler_json, "sampler_json");
+        need(index_out, "index_out");
+        need(gflops_out, "gflops_out");
+        need(count, "count");
+        GenerateReport rep;
+        std::vector<ConvDraw> draws;
+        auto recs = generate_conv_shard(CategoricalModel::from_json_text(sampler_json), conv_dist(dist),
+                                        conv_bounds(bounds_json), conv_hw(hw), n_samples, seed, rank, world,
+                                        opts_of(opts), checkpoint_path ? checkpoint_path : "", &draws, &rep);
+        shard_out(draws, recs, rep, inputs_out, tunings_out, index_out, gflops_out, cap, count, attempts, duplicates,
+                  unlaunchable, [](const ConvInput& x) { return out_in(x); },
+                  [](const ConvTuning& x) { return out_t(x); });
+    });
+}
+
+int ktune_shard_lpt(const double* costs, int64_t n, int32_t world, int32_t* rank_out) {
+    return guard([&] {
+        need(costs, "costs");
+        need(rank_out, "rank_out");
+        const auto shards = shard_lpt(std::vector<double>(costs, costs + n), world);
+        for (std::size_t r = 0; r < shards.size(); ++r)
+            for (std::int64_t i : shards[r]) rank_out[i] = int32_t(r);
     });
 }
 

@@ -13,6 +13,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <filesystem>
+#include <map>
+#include <fstream>
 #include <numeric>
 #include <set>
 #include <sstream>
@@ -151,9 +153,15 @@ std::size_t pick_shape(std::mt19937_64& rng, std::size_t n, const std::vector<do
 
 // The shared sample -> dedup loop of generate_*_dataset; `emit` receives
 // each distinct pair in order.
-template <typename In, typename Tu, typename Dist, typename Bounds, typename FromValues, typename Emit>
+// `accept` (may be empty) is the measuring backend's launchability filter:
+// rejected draws are redrawn and counted, never measured.
+constexpr int kUnlaunchableRedrawLimit = 1000000;
+
+template <typename In, typename Tu, typename Dist, typename Bounds, typename FromValues, typename Emit,
+          typename Accept>
 void draw_distinct(const CategoricalModel& model, const Dist& dist, const Bounds& bounds, const HardwareDescriptor& hw,
-                   int n_samples, std::uint64_t seed, GenerateReport* report, FromValues from_values, Emit emit) {
+                   int n_samples, std::uint64_t seed, GenerateReport* report, FromValues from_values, Emit emit,
+                   const Accept& accept) {
     if (n_samples < 1) throw std::invalid_argument("n_samples must be >= 1");
     dist.validate();
     model.validate();
@@ -162,6 +170,7 @@ void draw_distinct(const CategoricalModel& model, const Dist& dist, const Bounds
     std::set<std::string> seen;
     GenerateReport rep;
     int consecutive = 0;
+    int unlaunchable_run = 0;
     int produced = 0;
     while (produced < n_samples) {
         const In input = dist.draw(rng);
@@ -169,6 +178,14 @@ void draw_distinct(const CategoricalModel& model, const Dist& dist, const Bounds
         const std::vector<int> vals = sample(model, legal, rng);
         ++rep.attempts;
         const Tu tuning = from_values(vals);
+        if (accept && !accept(input, tuning)) {
+            ++rep.unlaunchable_rejected;
+            if (++unlaunchable_run > kUnlaunchableRedrawLimit)
+                throw std::runtime_error("dataset generation stalled: " + std::to_string(kUnlaunchableRedrawLimit) +
+                                         " consecutive draws the backend cannot launch");
+            continue;
+        }
+        unlaunchable_run = 0;
         if (!seen.insert(key_of(input, tuning)).second) {
             ++rep.duplicates_rejected;
             if (++consecutive > kDuplicateRedrawLimit)
@@ -383,22 +400,158 @@ ConvInput ConvInputDistribution::draw(std::mt19937_64& rng) const {
 
 std::vector<GemmDraw> predraw_gemm(const CategoricalModel& model, const GemmInputDistribution& dist,
                                    const GemmBounds& bounds, const HardwareDescriptor& hw, int n_samples,
-                                   std::uint64_t seed, GenerateReport* report) {
+                                   std::uint64_t seed, GenerateReport* report, const GemmAccept& accept) {
     std::vector<GemmDraw> out;
     out.reserve(std::size_t(std::max(n_samples, 0)));
     draw_distinct<GemmInput, GemmTuning>(model, dist, bounds, hw, n_samples, seed, report, gemm_tuning_from_values,
-                                         [&](const GemmInput& in, const GemmTuning& t) { out.push_back({in, t}); });
+                                         [&](const GemmInput& in, const GemmTuning& t) { out.push_back({in, t}); },
+                                         accept);
     return out;
 }
 
 std::vector<ConvDraw> predraw_conv(const CategoricalModel& model, const ConvInputDistribution& dist,
                                    const ConvBounds& bounds, const HardwareDescriptor& hw, int n_samples,
-                                   std::uint64_t seed, GenerateReport* report) {
+                                   std::uint64_t seed, GenerateReport* report, const ConvAccept& accept) {
     std::vector<ConvDraw> out;
     out.reserve(std::size_t(std::max(n_samples, 0)));
     draw_distinct<ConvInput, ConvTuning>(model, dist, bounds, hw, n_samples, seed, report, conv_tuning_from_values,
-                                         [&](const ConvInput& in, const ConvTuning& t) { out.push_back({in, t}); });
+                                         [&](const ConvInput& in, const ConvTuning& t) { out.push_back({in, t}); },
+                                         accept);
     return out;
+}
+
+std::vector<std::vector<std::int64_t>> shard_lpt(const std::vector<double>& costs, int world) {
+    if (world < 1) throw std::invalid_argument("shard_lpt: world size must be >= 1");
+    std::vector<std::int64_t> order(costs.size());
+    std::iota(order.begin(), order.end(), std::int64_t(0));
+    std::stable_sort(order.begin(), order.end(), [&](std::int64_t a, std::int64_t b) { return costs[a] > costs[b]; });
+    std::vector<double> load(static_cast<std::size_t>(world), 0.0);
+    std::vector<std::vector<std::int64_t>> shards(static_cast<std::size_t>(world));
+    for (std::int64_t i : order) {
+        const auto r = std::size_t(std::min_element(load.begin(), load.end()) - load.begin());
+        shards[r].push_back(i);
+        load[r] += costs[std::size_t(i)];
+    }
+    for (auto& sh : shards) std::sort(sh.begin(), sh.end());
+    return shards;
+}
+
+namespace {
+
+double flops_of(const GemmInput& in) { return 2.0 * double(in.m) * double(in.n) * double(in.k); }
+double flops_of(const ConvInput& in) {
+    return 2.0 * double(in.n_batch) * double(in.p) * double(in.q) * double(in.k_filters) * double(in.c) *
+           double(in.r) * double(in.s);
+}
+
+// Checkpoint of one rank: a header line, then "index,gflops" per measured
+// sample, appended batch by batch (a killed run resumes where it stopped).
+std::string shard_header(const char* kind, int rank, int world, int n, std::uint64_t seed, const MeasureOptions& o) {
+    std::ostringstream h;
+    h << "ktune-shard-1 " << kind << " rank=" << rank << " world=" << world << " n=" << n << " seed=" << seed
+      << " mode=" << int(o.mode) << " reps=" << o.repetitions;
+    return h.str();
+}
+
+std::map<std::int64_t, double> read_checkpoint(const std::string& path, const std::string& header) {
+    std::map<std::int64_t, double> done;
+    if (path.empty() || !std::filesystem::exists(path)) return done;
+    std::ifstream in(path);
+    std::string line;
+    if (!std::getline(in, line) || line != header)
+        throw std::runtime_error("checkpoint " + path + " belongs to a different run (header mismatch)");
+    while (std::getline(in, line)) {
+        const auto comma = line.find(',');
+        if (comma == std::string::npos) continue;  // a torn last line of a killed run
+        try {
+            done[std::stoll(line.substr(0, comma))] = std::stod(line.substr(comma + 1));
+        } catch (const std::exception&) {
+            continue;
+        }
+    }
+    return done;
+}
+
+template <typename Draw, typename MeasureMany>
+std::vector<ShardRecord> run_shard(const char* kind, const std::vector<Draw>& draws, int n_samples,
+                                   std::uint64_t seed, int rank, int world, const MeasureOptions& opt,
+                                   const std::string& checkpoint, MeasureMany measure_many) {
+    if (rank < 0 || rank >= world) throw std::invalid_argument("shard: rank must lie in [0, world)");
+    std::vector<double> cost(draws.size());
+    for (std::size_t i = 0; i < draws.size(); ++i) cost[i] = flops_of(draws[i].input);
+    const auto shards = shard_lpt(cost, world);
+    const std::string header = shard_header(kind, rank, world, n_samples, seed, opt);
+    std::map<std::int64_t, double> done = read_checkpoint(checkpoint, header);
+    std::vector<std::int64_t> todo;
+    for (std::int64_t i : shards[std::size_t(rank)])
+        if (!done.count(i)) todo.push_back(i);
+    std::ofstream ck;
+    if (!checkpoint.empty()) {
+        const bool fresh = !std::filesystem::exists(checkpoint) || done.empty();
+        ck.open(checkpoint, fresh ? std::ios::trunc : std::ios::app);
+        if (!ck) throw std::runtime_error("cannot write checkpoint " + checkpoint);
+        if (fresh) ck << header << '\n' << std::flush;
+    }
+    constexpr std::size_t kBatch = 64;
+    for (std::size_t b = 0; b < todo.size(); b += kBatch) {
+        const std::size_t e = std::min(todo.size(), b + kBatch);
+        std::vector<std::int64_t> idx(todo.begin() + std::ptrdiff_t(b), todo.begin() + std::ptrdiff_t(e));
+        const std::vector<double> g = measure_many(idx);
+        for (std::size_t j = 0; j < idx.size(); ++j) {
+            done[idx[j]] = g[j];
+            if (ck.is_open()) ck << idx[j] << ',' << fmt_double(g[j]) << '\n';
+        }
+        if (ck.is_open()) ck << std::flush;
+    }
+    std::vector<ShardRecord> out;
+    for (std::int64_t i : shards[std::size_t(rank)]) out.push_back({i, done.at(i)});
+    return out;
+}
+
+}  // namespace
+
+std::vector<ShardRecord> generate_gemm_shard(const CategoricalModel& model, const GemmInputDistribution& dist,
+                                             const GemmBounds& bounds, const HardwareDescriptor& hw, int n_samples,
+                                             std::uint64_t seed, int rank, int world, const MeasureOptions& opt,
+                                             const std::string& checkpoint, std::vector<GemmDraw>* draws,
+                                             GenerateReport* report) {
+    B200Backend backend(hw, opt);
+    auto seq = predraw_gemm(model, dist, bounds, hw, n_samples, seed, report,
+                            GemmAccept([&](const GemmInput& in, const GemmTuning& t) { return backend.accepts(in, t); }));
+    auto recs = run_shard("gemm", seq, n_samples, seed, rank, world, opt, checkpoint,
+                          [&](const std::vector<std::int64_t>& idx) {
+                              std::vector<GemmInput> in;
+                              std::vector<GemmTuning> tu;
+                              for (std::int64_t i : idx) {
+                                  in.push_back(seq[std::size_t(i)].input);
+                                  tu.push_back(seq[std::size_t(i)].tuning);
+                              }
+                              return measure_gemm_many(hw, in, tu, opt);
+                          });
+    if (draws) *draws = std::move(seq);
+    return recs;
+}
+
+std::vector<ShardRecord> generate_conv_shard(const CategoricalModel& model, const ConvInputDistribution& dist,
+                                             const ConvBounds& bounds, const HardwareDescriptor& hw, int n_samples,
+                                             std::uint64_t seed, int rank, int world, const MeasureOptions& opt,
+                                             const std::string& checkpoint, std::vector<ConvDraw>* draws,
+                                             GenerateReport* report) {
+    B200Backend backend(hw, opt);
+    auto seq = predraw_conv(model, dist, bounds, hw, n_samples, seed, report,
+                            ConvAccept([&](const ConvInput& in, const ConvTuning& t) { return backend.accepts(in, t); }));
+    auto recs = run_shard("conv", seq, n_samples, seed, rank, world, opt, checkpoint,
+                          [&](const std::vector<std::int64_t>& idx) {
+                              std::vector<ConvInput> in;
+                              std::vector<ConvTuning> tu;
+                              for (std::int64_t i : idx) {
+                                  in.push_back(seq[std::size_t(i)].input);
+                                  tu.push_back(seq[std::size_t(i)].tuning);
+                              }
+                              return measure_conv_many(hw, in, tu, opt);
+                          });
+    if (draws) *draws = std::move(seq);
+    return recs;
 }
 
 GemmDataset generate_gemm_dataset(MeasurementBackend& backend, const CategoricalModel& sampler_model,
@@ -412,7 +565,8 @@ GemmDataset generate_gemm_dataset(MeasurementBackend& backend, const Categorical
             const double g = backend.measure(in, t);
             if (!(std::isfinite(g) && g > 0.0)) throw std::runtime_error("backend returned non-positive gflops");
             ds.samples.push_back({in, t, g, backend.name(), wall_ms()});
-        });
+        },
+        GemmAccept([&](const GemmInput& in, const GemmTuning& t) { return backend.accepts(in, t); }));
     return ds;
 }
 
@@ -427,7 +581,8 @@ ConvDataset generate_conv_dataset(MeasurementBackend& backend, const Categorical
             const double g = backend.measure(in, t);
             if (!(std::isfinite(g) && g > 0.0)) throw std::runtime_error("backend returned non-positive gflops");
             ds.samples.push_back({in, t, g, backend.name(), wall_ms()});
-        });
+        },
+        ConvAccept([&](const ConvInput& in, const ConvTuning& t) { return backend.accepts(in, t); }));
     return ds;
 }
 

@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "ktune/kernels.hpp"
 #include "ktune/space.hpp"
@@ -19,6 +20,11 @@ class MeasurementBackend {
     virtual std::string name() const = 0;
     virtual double measure(const GemmInput& in, const GemmTuning& t) = 0;
     virtual double measure(const ConvInput& in, const ConvTuning& t) = 0;
+    // Whether measure() can run this legal pair (the reference's executors
+    // run every legal tuple: default true).  generate_*_dataset redraws the
+    // pairs a backend does not accept instead of aborting on them.
+    virtual bool accepts(const GemmInput&, const GemmTuning&) const { return true; }
+    virtual bool accepts(const ConvInput&, const ConvTuning&) const { return true; }
 };
 
 struct MeasureOptions {
@@ -42,6 +48,16 @@ MeasureResult measure_gemm_device(const HardwareDescriptor& hw, const GemmInput&
 MeasureResult measure_conv_device(const HardwareDescriptor& hw, const ConvInput& in, const ConvTuning& t,
                                   const MeasureOptions& opt);
 
+// Many measurements with one host synchronisation per call: every pair's
+// warm-up and timed repetitions (each after an L2 flush) are enqueued back to
+// back with their CUDA events, then all events are read once.  Same protocol
+// and result as measure_*_device per pair; a pair that fails to launch
+// (unsupported by this build) yields -1 instead of aborting the batch.
+std::vector<double> measure_gemm_many(const HardwareDescriptor& hw, const std::vector<GemmInput>& in,
+                                      const std::vector<GemmTuning>& t, const MeasureOptions& opt);
+std::vector<double> measure_conv_many(const HardwareDescriptor& hw, const std::vector<ConvInput>& in,
+                                      const std::vector<ConvTuning>& t, const MeasureOptions& opt);
+
 class B200Backend final : public MeasurementBackend {
   public:
     explicit B200Backend(HardwareDescriptor hw, MeasureOptions opt = {});
@@ -49,6 +65,9 @@ class B200Backend final : public MeasurementBackend {
     std::string name() const override { return opt_.mode == dev::Mode::parity ? "b200-parity" : "b200"; }
     double measure(const GemmInput& in, const GemmTuning& t) override;
     double measure(const ConvInput& in, const ConvTuning& t) override;
+    // inside this build's launch envelope (host-side planning, no launch)
+    bool accepts(const GemmInput& in, const GemmTuning& t) const override;
+    bool accepts(const ConvInput& in, const ConvTuning& t) const override;
     const HardwareDescriptor& hw() const { return hw_; }
 
   private:

@@ -27,6 +27,7 @@
 #include <set>
 #include <sstream>
 #include <stdexcept>
+#include <cmath>
 #include <string>
 #include <vector>
 
@@ -380,7 +381,83 @@ int do_calibrate(const Args& a) {
     return 0;
 }
 
+// --merge: the dataset CSV from the shard files of `generate --shard R/N`
+// (the file-based form of the all-gather: rows placed by sequence index).
+int do_merge(const Args& a, const std::string& out) {
+    std::vector<std::string> files;
+    {
+        std::stringstream ss(a.str("merge"));
+        std::string f;
+        while (std::getline(ss, f, ','))
+            if (!f.empty()) files.push_back(f);
+    }
+    std::string header, csv_header, kind;
+    std::map<long long, std::string> rows;
+    long long n = -1;
+    for (const auto& f : files) {
+        std::ifstream in(f);
+        if (!in) throw UsageError("cannot read shard file " + f);
+        std::string h, ch, line;
+        std::getline(in, h);
+        std::getline(in, ch);
+        if (h.rfind("ktune-shard-records-1 ", 0) != 0) throw UsageError(f + " is not a shard file");
+        std::istringstream hs(h);
+        std::string tag, k, nfield;
+        hs >> tag >> k >> nfield;
+        const long long nn = std::stoll(nfield.substr(nfield.find('=') + 1));
+        if (n >= 0 && (nn != n || k != kind || ch != csv_header)) throw UsageError(f + " belongs to another run");
+        n = nn;
+        kind = k;
+        csv_header = ch;
+        while (std::getline(in, line)) {
+            const auto c = line.find(',');
+            if (c == std::string::npos) continue;
+            rows[std::stoll(line.substr(0, c))] = line.substr(c + 1);
+        }
+    }
+    if (n < 0 || (long long)rows.size() != n)
+        throw UsageError("shards cover " + std::to_string(rows.size()) + " of " + std::to_string(n) + " samples");
+    std::ofstream o(out);
+    o << csv_header << '\n';
+    for (const auto& r : rows) o << r.second << '\n';
+    std::printf("merged %zu shard file(s): %lld %s samples to %s\n", files.size(), n, kind.c_str(), out.c_str());
+    return 0;
+}
+
+// --shard R/N: this rank's share of the sequence (LPT by 2MNK), measured on
+// the B200 with batched syncs and an optional resumable --checkpoint; writes
+// a shard file of "index,<dataset row>" lines for --merge.
+template <typename Draw, typename Dataset>
+void write_shard(const std::string& out, const std::string& kind, std::int64_t n, const std::vector<Draw>& draws,
+                 const std::vector<ShardRecord>& recs, const std::string& backend) {
+    Dataset one;
+    std::ofstream o(out);
+    if (!o) throw std::runtime_error("cannot write " + out);
+    std::string head;
+    {
+        Dataset empty;
+        head = to_csv_text(empty);
+        head = head.substr(0, head.find('\n'));
+    }
+    o << "ktune-shard-records-1 " << kind << " n=" << n << '\n' << head << '\n';
+    for (const auto& r : recs) {
+        if (!(std::isfinite(r.gflops) && r.gflops > 0.0))
+            throw std::runtime_error("sample " + std::to_string(r.index) + " failed to launch");
+        one.samples.clear();
+        one.samples.push_back({draws[std::size_t(r.index)].input, draws[std::size_t(r.index)].tuning, r.gflops,
+                               backend, 0});
+        std::string text = to_csv_text(one);
+        text = text.substr(text.find('\n') + 1);
+        while (!text.empty() && text.back() == '\n') text.pop_back();
+        o << r.index << ',' << text << '\n';
+    }
+}
+
 int do_generate(const Args& a) {
+    if (!a.str("merge").empty()) {
+        if (a.str("out").empty()) throw UsageError("pass --out <file> for the merged dataset CSV");
+        return do_merge(a, a.str("out"));
+    }
     const HardwareDescriptor hw = hw_from(a);
     const CategoricalModel sampler = sampler_from(a.str("sampler"));
     const std::string out = a.str("out");
@@ -407,6 +484,48 @@ int do_generate(const Args& a) {
            {"seed", seed}, {"backend", a.str("backend", "analytical")}};
     double lo = 0, hi = 0, sum = 0;
     std::size_t rows = 0;
+    int shard_rank = -1, shard_world = 0;
+    if (!a.str("shard").empty()) {
+        const std::string sh = a.str("shard");
+        const auto slash = sh.find('/');
+        if (slash == std::string::npos) throw UsageError("--shard expects R/N");
+        shard_rank = std::atoi(sh.substr(0, slash).c_str());
+        shard_world = std::atoi(sh.substr(slash + 1).c_str());
+        if (shard_world < 1 || shard_rank < 0 || shard_rank >= shard_world) throw UsageError("--shard R/N: 0 <= R < N");
+        const std::string be = a.str("backend", "analytical");
+        if (be != "b200" && be != "b200-parity") throw UsageError("--shard needs --backend b200 or b200-parity");
+        MeasureOptions opt;
+        opt.mode = be == "b200" ? dev::Mode::fast : dev::Mode::parity;
+        std::vector<ShardRecord> recs;
+        if (kind == "gemm") {
+            GemmInputDistribution dist;
+            dist.dtype = dtype;
+            dist.fixed_fraction = fraction;
+            for (const auto& s : shapes.gemm) dist.shapes.push_back(s.second);
+            std::vector<GemmDraw> draws;
+            recs = generate_gemm_shard(sampler, dist, bounds_from<GemmBounds>(a), hw, int(samples), seed, shard_rank,
+                                       shard_world, opt, a.str("checkpoint"), &draws, &rep);
+            write_shard<GemmDraw, GemmDataset>(out, kind, samples, draws, recs, be);
+        } else {
+            ConvInputDistribution dist;
+            dist.dtype = dtype;
+            dist.fixed_fraction = fraction;
+            for (const auto& s : shapes.conv) dist.shapes.push_back(s.second);
+            std::vector<ConvDraw> draws;
+            recs = generate_conv_shard(sampler, dist, bounds_from<ConvBounds>(a), hw, int(samples), seed, shard_rank,
+                                       shard_world, opt, a.str("checkpoint"), &draws, &rep);
+            write_shard<ConvDraw, ConvDataset>(out, kind, samples, draws, recs, be);
+        }
+        std::printf("shard %d/%d: wrote %zu of %lld %s samples to %s\n", shard_rank, shard_world, recs.size(),
+                    (long long)samples, kind.c_str(), out.c_str());
+        j["shard"] = {{"rank", shard_rank}, {"world", shard_world}, {"records", recs.size()}};
+        j["attempts"] = rep.attempts;
+        j["duplicates_rejected"] = rep.duplicates_rejected;
+        j["unlaunchable_rejected"] = rep.unlaunchable_rejected;
+        j["outputs"] = {{"shard", out}};
+        emit_report(a.str("report"), j, {{"seconds", wall_s() - t0}});
+        return 0;
+    }
     if (kind == "gemm") {
         const auto bounds = bounds_from<GemmBounds>(a);
         GemmInputDistribution dist;
@@ -644,7 +763,10 @@ const std::map<std::string, Verb>& verbs() {
            {"shape-fraction", false, "probability of drawing a fixture shape"},
            {"backend", false, "analytical|b200|b200-parity"}, {"dtype", false, "f32|f64|bf16|f16|tf32"},
            {"samples", false, "number of samples"}, {"seed", false, "rng seed (default 0)"},
-           {"out", false, "dataset CSV output path"}, {"report", false, "JSON report path"}},
+           {"out", false, "dataset CSV output path"}, {"report", false, "JSON report path"},
+           {"shard", false, "R/N: measure rank R's share of N (b200 backends); --out gets a shard file"},
+           {"checkpoint", false, "resumable per-rank progress file for --shard"},
+           {"merge", false, "comma list of shard files: write the merged dataset to --out"}},
           do_generate}},
         {"train",
          {"fit the MLP performance model",

@@ -224,44 +224,79 @@ def shard_lpt(costs, world_size: int) -> list:
 
 def generate_sharded(sampler_json: str, dist, hw: HardwareDescriptor, bounds_json: str | None, n_samples: int,
                      seed: int, backend: str = "b200", mode: str = "fast", repetitions: int = 3, group=None,
-                     device=None):
-    """Sharded generate_*_dataset: every rank pre-draws the same sequence,
-    measures its LPT shard, and one all-gather of fixed-size records
-    {index, gflops} (NCCL over NVLink on GPUs, gloo on CPU) rebuilds the
-    dataset in canonical order on every rank.  Returns (csv_text, stats)."""
+                     device=None, checkpoint: str | None = None):
+    """Sharded generate_*_dataset (pipeline.cpp:463-556).
+
+    Every rank pre-draws the same sequence and measures its LPT shard -- on
+    the b200 backend inside the library (ktune_generate_*_shard: batched
+    device timing, one host sync per batch, optional resumable checkpoint
+    file per rank); then one all-gather of fixed-size {index, gflops} records
+    (NCCL over NVLink on GPUs, gloo on CPU) rebuilds the dataset in canonical
+    order on every rank.  A rank whose measurements fail still reaches the
+    collective (its failure travels in the records), and every rank raises
+    after the gather, so no rank is left blocked.  Returns (csv_text, stats)."""
     import torch
     import torch.distributed as dist_
 
     ws = dist_.get_world_size(group) if dist_.is_initialized() else 1
     rank = dist_.get_rank(group) if dist_.is_initialized() else 0
+    conv = isinstance(dist, ConvInputDistribution)
     t0 = time.perf_counter()
-    ins, tus, att, dup = predraw(sampler_json, dist, hw, bounds_json, n_samples, seed)
-    t_draw = time.perf_counter() - t0
-    shards = shard_lpt([flops_of(x) for x in ins], ws)
-    mine = shards[rank]
-    py_ins, py_tus = as_inputs(ins), as_tunings(tus)
-    t1 = time.perf_counter()
-    recs = np.zeros((len(mine), 2), np.float64)
-    for j, i in enumerate(mine):
-        if backend == "analytical":
-            g = analytical_gflops(py_ins[i], py_tus[i], hw)
-        else:
-            g = measure(py_ins[i], py_tus[i], hw, mode, repetitions=repetitions, warmup=1)
-        if not (np.isfinite(g) and g > 0):
-            raise RuntimeError("backend returned non-positive gflops")
-        recs[j] = (i, g)
-    t_measure = time.perf_counter() - t1
-    per = max(len(s) for s in shards)
-    buf = np.full((per, 2), -1.0)
-    buf[: len(mine)] = recs
+    error = None
+    unl = 0
+    if backend == "analytical":
+        ins, tus, att, dup = predraw(sampler_json, dist, hw, bounds_json, n_samples, seed)
+        t_draw = time.perf_counter() - t0
+        owner = shard_lpt_owner([flops_of(x) for x in ins], ws)
+        mine = [i for i in range(n_samples) if owner[i] == rank]
+        py_ins, py_tus = as_inputs(ins), as_tunings(tus)
+        recs = np.zeros((len(mine), 2), np.float64)
+        for j, i in enumerate(mine):
+            recs[j] = (i, analytical_gflops(py_ins[i], py_tus[i], hw))
+        t_measure = time.perf_counter() - t0 - t_draw
+    else:
+        d, keep = dist.c()
+        ins = ((_lib.ConvInputC if conv else _lib.GemmInputC) * n_samples)()
+        tus = ((_lib.ConvTuningC if conv else _lib.GemmTuningC) * n_samples)()
+        cap = n_samples
+        idx = np.zeros(cap, np.int64)
+        gfl = np.zeros(cap, np.float64)
+        cnt, att_, dup_, unl_ = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        opts = _lib.MeasureOptionsC(_lib.MODE_FAST if mode == "fast" else _lib.MODE_PARITY, repetitions, 1, 1, 0x5EED)
+        try:
+            _lib.call("ktune_generate_conv_shard" if conv else "ktune_generate_gemm_shard", ctypes.byref(hw.c()),
+                      _b(bounds_json or ""), sampler_json.encode(), ctypes.byref(d), n_samples, seed, rank, ws,
+                      ctypes.byref(opts), None if checkpoint is None else checkpoint.encode(),
+                      ctypes.cast(ins, ctypes.c_void_p), ctypes.cast(tus, ctypes.c_void_p),
+                      idx.ctypes.data_as(ctypes.c_void_p), gfl.ctypes.data_as(ctypes.c_void_p), cap,
+                      ctypes.byref(cnt), ctypes.byref(att_), ctypes.byref(dup_), ctypes.byref(unl_))
+            recs = np.stack([idx[: cnt.value].astype(np.float64), gfl[: cnt.value]], axis=1)
+        except Exception as e:  # noqa: BLE001 -- reported to every rank after the gather
+            error = f"rank {rank}: {e}"
+            recs = np.zeros((0, 2))
+        del keep
+        att, dup, unl = att_.value, dup_.value, unl_.value
+        t_draw = float("nan")
+        t_measure = time.perf_counter() - t0
+    # fixed-size records: rank r sends at most ceil(n / ws) + the LPT excess;
+    # an all-reduce of the local count sizes the buffer exactly
+    n_local = torch.tensor([len(recs), 1 if error else 0], dtype=torch.int64)
     if ws > 1:
         dev = device if device is not None else ("cuda" if dist_.get_backend(group) == "nccl" else "cpu")
+        n_local = n_local.to(dev)
+        dist_.all_reduce(n_local, op=dist_.ReduceOp.MAX, group=group)
+        per, failed = int(n_local[0].item()), int(n_local[1].item())
+        buf = np.full((per, 2), -1.0)
+        buf[: len(recs)] = recs
         local = torch.from_numpy(buf).to(dev)
         gathered = torch.empty((ws * per, 2), dtype=torch.float64, device=dev)
         dist_.all_gather_into_tensor(gathered, local, group=group)
         allrec = gathered.cpu().numpy()
     else:
-        allrec = buf
+        failed = 1 if error else 0
+        allrec = recs
+    if failed:
+        raise RuntimeError(error or "sharded generation failed on another rank")
     gflops = np.zeros(n_samples)
     seen = np.zeros(n_samples, bool)
     for i, g in allrec:
@@ -270,11 +305,23 @@ def generate_sharded(sampler_json: str, dist, hw: HardwareDescriptor, bounds_jso
             seen[int(i)] = True
     if not seen.all():
         raise RuntimeError("sharded generation lost records")
+    if not (np.isfinite(gflops) & (gflops > 0)).all():
+        raise RuntimeError("backend returned non-positive gflops")
     name = backend if backend != "b200" or mode == "fast" else "b200-parity"
     text = dataset_csv(ins, tus, gflops, name)
-    stats = {"attempts": att, "duplicates": dup, "predraw_s": t_draw, "measure_s": t_measure,
-             "local_samples": len(mine), "world_size": ws}
+    stats = {"attempts": att, "duplicates": dup, "unlaunchable": unl, "predraw_s": t_draw, "measure_s": t_measure,
+             "local_samples": len(recs), "world_size": ws}
     return text, stats
+
+
+def shard_lpt_owner(costs, world_size: int) -> np.ndarray:
+    """owner[i] = rank of sample i under the library's LPT assignment
+    (ktune_shard_lpt; same rule as shard_lpt below)."""
+    c = np.ascontiguousarray(costs, np.float64)
+    out = np.zeros(len(c), np.int32)
+    _lib.call("ktune_shard_lpt", c.ctypes.data_as(ctypes.c_void_p), len(c), world_size,
+              out.ctypes.data_as(ctypes.c_void_p))
+    return out
 
 
 # ---------------------------------------------------------------------------
