@@ -202,7 +202,7 @@ def cpu_baseline_sample(tuple_):
     if lib is not None:
         tv = (ctypes.c_int32 * 8)(*tuple_)
         g, s = ctypes.c_double(), ctypes.c_double()
-        reps = int(os.environ.get("KTUNE_CPU_REPS", "8"))
+        reps = int(os.environ.get("KTUNE_CPU_REPS", "160"))  # ~10 s of host work
         rc = lib.ref_host_gemm_gflops(ctypes.c_int64(w["m"]), ctypes.c_int64(w["n"]), ctypes.c_int64(w["k"]), 0, 0, tv,
                                       reps, threads, ctypes.byref(g), ctypes.byref(s))
         if rc != 0:
@@ -355,6 +355,8 @@ def ref_tuning_baseline(ins, tus, hw_json, budget_s=20.0):
     the sequence's mean FLOP per sample)."""
     import ctypes
     from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_libs as O
     lib = O.reference()
@@ -376,7 +378,7 @@ def ref_tuning_baseline(ins, tus, hw_json, budget_s=20.0):
         x, t = ins[i], tus[i]
         tv = (ctypes.c_int32 * 8)(t.m_s, t.n_s, t.m_l, t.n_l, t.u, t.k_s, t.k_l, t.k_g)
         g = ctypes.c_double()
-        if fn(hwj, x.m, x.n, x.k, 1, x.trans_a, x.trans_b, tv, 3, ctypes.byref(g)) == 0:
+        if fn(hwj, x.m, x.n, x.k, 1, int(x.trans_a), int(x.trans_b), tv, 3, ctypes.byref(g)) == 0:
             done_flops[0] += 4 * flops[i]
             done[0] += 1
 
@@ -424,7 +426,10 @@ def tuning_loop(args, ws, rank, dev):
     if ws > 1:
         dist.all_reduce(el, op=dist.ReduceOp.MAX)
     secs = float(el[0].item())
+    rows = [line.split(",") for line in csv.strip().splitlines()[1:]]
+    dev_s = sum(4 * 2.0 * float(r[0]) * float(r[1]) * float(r[2]) / (float(r[14]) * 1e9) for r in rows)
     out = {"samples": n, "samples_per_s": n / secs, "seconds": secs, "n_gpus": ws,
+           "device_seconds_est": dev_s,  # sum of warm-up + 3 reps at each sample's best time (all ranks)
            "scaling": "strong (fixed pre-drawn sequence, LPT-sharded by 2MNK)",
            "unlaunchable_redrawn": stats["unlaunchable"], "local_samples": stats["local_samples"],
            "gather": "NCCL all_gather_into_tensor of {index, gflops} records" if ws > 1 else "single rank",
@@ -924,7 +929,7 @@ def main():
     ap.add_argument("--candidates", type=int, default=3000)
     ap.add_argument("--pick", default="", help="fixed tuple m_s,n_s,m_l,n_l,u,k_s,k_l,k_g (skips selection)")
     ap.add_argument("--no-extras", action="store_true", help="headline only (no tuning loop / other configs)")
-    ap.add_argument("--tuning-samples", type=int, default=10000,
+    ap.add_argument("--tuning-samples", type=int, default=4000,
                     help="tuning-loop samples in total (fixed pre-drawn sequence, sharded over the GPUs)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

@@ -100,6 +100,7 @@ int ktune_enumerate_legal_gemm(const ktune_hw* hw, const ktune_gemm_input* in, c
                                ktune_gemm_tuning* out, int64_t cap, int64_t* count) {
     return guard([&] {
         need(count, "count");
+        if (cap > 0) need(out, "out");
         GemmBounds b = (bounds_json && bounds_json[0]) ? GemmBounds::from_json_text(bounds_json) : GemmBounds::defaults();
         auto list = enumerate_legal(conv_in(in), conv_hw(hw), b);
         *count = int64_t(list.size());
@@ -114,6 +115,7 @@ int ktune_enumerate_legal_conv(const ktune_hw* hw, const ktune_conv_input* in, c
                                ktune_conv_tuning* out, int64_t cap, int64_t* count) {
     return guard([&] {
         need(count, "count");
+        if (cap > 0) need(out, "out");
         ConvBounds b = (bounds_json && bounds_json[0]) ? ConvBounds::from_json_text(bounds_json) : ConvBounds::defaults();
         auto list = enumerate_legal(conv_in(in), conv_hw(hw), b);
         *count = int64_t(list.size());
@@ -143,6 +145,7 @@ int ktune_encode_features_conv(const ktune_conv_input* in, const ktune_conv_tuni
 int ktune_build_indirection_table(const ktune_conv_input* in, int64_t* out4, int64_t cap, int64_t* count) {
     return guard([&] {
         need(count, "count");
+        if (cap > 0) need(out4, "out4");
         auto tab = build_indirection_table(conv_in(in));
         *count = int64_t(tab.size());
         for (int64_t i = 0; i < std::min<int64_t>(cap, *count); ++i) {
@@ -257,6 +260,8 @@ int ktune_tensor_write(const char* path, int32_t dtype, const int64_t* dims, int
         TensorFile t;
         t.dtype = dtype_of(dtype);
         if (ndims < 0 || (ndims > 0 && dims == nullptr)) throw std::invalid_argument("tensor_write: bad dims");
+        for (int32_t i = 0; i < ndims; ++i)
+            if (dims[i] < 1) throw std::invalid_argument("tensor_write: every dim must be >= 1");
         t.dims.assign(dims, dims + ndims);
         const std::int64_t n = ndims > 0 ? t.element_count() : 0;
         if (n > 0) need(data, "data");

@@ -496,7 +496,13 @@ int ktune_select_gemm(const ktune_hw* hw, const char* bounds_json, const char* m
     return guard([&] {
         need(chosen, "chosen");
         const GemmInput input = conv_in(in);
-        const std::string key = cache_key(input);
+        // the in-memory argmax is valid only for the configuration that
+        // filled it: the key covers the input signature, the hardware
+        // descriptor, the bounds, the predictor model and top_k
+        const HardwareDescriptor hwd = conv_hw(hw);
+        const std::string key = cache_key(input) + "|" + fnv1a64_hex(hwd.to_json_text()) + "|" +
+                                fnv1a64_hex(bounds_json ? bounds_json : "") + "|" +
+                                fnv1a64_hex(model_json ? model_json : "") + "|" + std::to_string(top_k);
         {
             std::lock_guard<std::mutex> lock(g_select_mu);
             auto it = g_select_memo.find(key);

@@ -814,16 +814,6 @@ Result result_of(const std::string& text, const char* kind, const std::vector<st
     }
 }
 
-std::string fnv1a64_hex(const std::string& text) {
-    std::uint64_t h = 0xcbf29ce484222325ULL;
-    for (unsigned char c : text) {
-        h ^= c;
-        h *= 0x100000001b3ULL;
-    }
-    char buf[17];
-    std::snprintf(buf, sizeof(buf), "%016llx", static_cast<unsigned long long>(h));
-    return buf;
-}
 
 std::string descriptor(const GemmInput& in) {
     std::ostringstream s;
@@ -871,6 +861,17 @@ GemmInferenceResult gemm_result_from_json_text(const std::string& text) {
 ConvInferenceResult conv_result_from_json_text(const std::string& text) {
     return result_of<ConvInferenceResult, ConvCandidate>(text, "conv", conv_param_names(), conv_input_of,
                                                          conv_tuning_from_values);
+}
+
+std::string fnv1a64_hex(const std::string& text) {
+    std::uint64_t h = 0xcbf29ce484222325ULL;
+    for (unsigned char c : text) {
+        h ^= c;
+        h *= 0x100000001b3ULL;
+    }
+    char buf[17];
+    std::snprintf(buf, sizeof(buf), "%016llx", static_cast<unsigned long long>(h));
+    return buf;
 }
 
 std::string cache_key(const GemmInput& input) { return "gemm-" + fnv1a64_hex(descriptor(input)) + ".json"; }
