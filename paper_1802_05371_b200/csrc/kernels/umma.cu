@@ -17,8 +17,10 @@
 //         (tcgen05.mma.cta_group::2, 128 rows per CTA)
 //   n_l   BLOCK_N = UMMA_N (16..256)
 //   u     BLOCK_K elements per pipeline stage (>= 32 bytes)
-//   k_g   split-K slices over the grid (deterministic ordered fix-up, as
-//         in the SIMT family)
+//   k_g   split-K degree: k_g > 1 runs stream-K over min(SMs, tiles * k_g)
+//         CTAs (equal contiguous shares of the (tile, k-block) iterations;
+//         split tiles folded by the last-arriving segments, two levels,
+//         deterministic order)
 //   k_s   TMEM accumulator buffers (1, or 2 = the epilogue of one tile
 //         overlaps the MMAs of the next in the persistent schedule)
 //   n_s   rasterisation width: concurrent CTAs sweep n_s column tiles
@@ -47,7 +49,10 @@ struct TcParams {
     int bm, bn, bk;
     int tile_m;                   // output rows per tile: 128, or 256 for a CTA pair
     int stages;
-    int kb_total, kb_span, nz;
+    int kb_total;                 // k-blocks per tile
+    int streamk;                  // k_g > 1: balanced contiguous (tile, k-block) ranges per CTA
+    long long total_it;           // tiles * kb_total (stream-K iteration space)
+    int smax, gmax;               // stream-K: max segments per tile, max fold groups per tile
     int a_kmajor, b_kmajor;
     int a_sw, b_sw;               // swizzle span (bytes) of each operand's tiles
     int a_boxes, b_boxes;         // TMA boxes per stage
@@ -62,9 +67,9 @@ struct TcParams {
     int tiles_m, tiles_n;         // output tile grid
     int raster;                   // rasterisation group width in n-tiles
     float* C;
-    float* ws;
-    unsigned long long* flags;
-    unsigned long long token;
+    float* ws;                    // [smax][M*N] segment partials (C layout)
+    float* ws2;                   // [gmax][M*N] fold-group partials
+    unsigned* counters;           // zeroed: [tiles * (pair ? 2 : 1)][gmax + 1] arrival counters
     unsigned a_desc_hi, b_desc_hi;    // SBO | version | layout (descriptor bits 32..63)
     unsigned a_desc_lbo, b_desc_lbo;  // LBO field in place (descriptor bits 16..29)
     unsigned a_koff[8], b_koff[8];    // byte offset of UMMA_K slice kk inside a stage tile
@@ -101,10 +106,10 @@ __device__ __forceinline__ void probe_kb(const TcParams& p, int i, int slot) {
     p.dbg[64 + (blockIdx.x * 64 + i) * 4 + slot] = (long long)t;
 }
 
-__device__ __forceinline__ Unit unit_of(const TcParams& p, int u) {
+// Output tile t in raster order -> (m0, n0, tile id).
+__device__ __forceinline__ Unit unit_of(const TcParams& p, int t) {
     Unit w;
-    w.g = u % p.nz;
-    const int t = u / p.nz;
+    w.g = 0;
     const int per_group = p.raster * p.tiles_m;
     const int group = t / per_group;
     const int cols = min(p.raster, p.tiles_n - group * p.raster);
@@ -115,6 +120,53 @@ __device__ __forceinline__ Unit unit_of(const TcParams& p, int u) {
     w.n0 = nt * p.bn;
     w.tile = mt * p.tiles_n + nt;
     return w;
+}
+
+// ---- stream-K work split (k_g > 1) -------------------------------------------
+// The (tile, k-block) iterations of the whole GEMM, tile-major in raster
+// order, are cut into G equal contiguous ranges, one per CTA (or pair): every
+// SM streams the same number of k-blocks whatever the tile count.  A range
+// that covers part of a tile produces a segment; segment j of tile t is the
+// one starting in CTA cfind(t*kbt) + j.  Segments of a split tile publish
+// partials; the last to arrive in each fold group of kFoldGroup segments
+// folds them (segment order), and the last group folds the groups (group
+// order) into C: a deterministic two-level fold with no waiting.
+constexpr int kFoldGroup = 8;
+
+struct Seg {
+    int m0, n0, tile;
+    int kb0, kb1;  // k-block range inside the tile
+    int j, S;      // segment index within the tile, segments of the tile
+};
+
+// last CTA whose range starts at or before iteration i
+__device__ __forceinline__ int cfind(long long i, long long T, int G) {
+    return int(((i + 1) * G - 1) / T);
+}
+
+template <class F>
+__device__ __forceinline__ void for_each_seg(const TcParams& p, int cta, int ncta, F&& fn) {
+    const int tiles = p.tiles_m * p.tiles_n;
+    if (!p.streamk) {
+        for (int t = cta; t < tiles; t += ncta) {
+            const Unit w = unit_of(p, t);
+            fn(Seg{w.m0, w.n0, w.tile, 0, p.kb_total, 0, 1});
+        }
+        return;
+    }
+    const long long T = p.total_it;
+    const int kbt = p.kb_total;
+    long long it = (long long)cta * T / ncta;
+    const long long e = (long long)(cta + 1) * T / ncta;
+    while (it < e) {
+        const int t = int(it / kbt);
+        const int kb0 = int(it - (long long)t * kbt);
+        const int kb1 = int(min((long long)kbt, kb0 + (e - it)));
+        const int c0 = cfind((long long)t * kbt, T, ncta);
+        const Unit w = unit_of(p, t);
+        fn(Seg{w.m0, w.n0, w.tile, kb0, kb1, cta - c0, cfind((long long)(t + 1) * kbt - 1, T, ncta) - c0 + 1});
+        it += kb1 - kb0;
+    }
 }
 
 // PAIR: a cluster of two CTAs on one TPC computes a 256-row tile with
@@ -149,7 +201,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
-    const int n_units = p.tiles_m * p.tiles_n * p.nz;
     const unsigned rank = PAIR ? cluster_ctarank() : 0u;
     const int cta = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);   // pair (or CTA) index
     const int ncta = PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
@@ -198,15 +249,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int a_row = PAIR ? int(rank) * 128 : 0;                 // this CTA's rows of the tile
         const int b_col = PAIR ? int(rank) * (p.bn / 2) : 0;          // this CTA's half of the columns
         int dbg_i = 0;
-        for (int u = cta; u < n_units; u += ncta) {
-            const Unit w = unit_of(p, u);
-            const int kb_begin = w.g * p.kb_span;
-            const int kb_end = min(p.kb_total, kb_begin + p.kb_span);
-            for (int kb = kb_begin; kb < kb_end; ++kb, ++dbg_i) {
+        bool first = true;
+        for_each_seg(p, cta, ncta, [&](const Seg& w) {
+            for (int kb = w.kb0; kb < w.kb1; ++kb, ++dbg_i) {
                 mbar_wait(empty + stage, phase ^ 1u);
                 if (lane == 0) probe_kb(p, dbg_i, 0);
                 if (elect_one()) {
-                    if (kb == kb_begin && u == cta) probe(p, 2);
+                    if (first) probe(p, 2);
+                    first = false;
                     unsigned char* sa = smem + std::size_t(stage) * stage_bytes;
                     unsigned char* sb = sa + p.a_tile_bytes;
                     const int k0 = kb * p.bk;
@@ -247,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     phase ^= 1u;
                 }
             }
-        }
+        });
     } else if (warp == 1) {
         // ---------------- MMA issuer (whole warp loops, one lane issues) ----------------
         // Descriptors: constant high words and k-slice offsets come from the
@@ -262,10 +312,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             unsigned acc_phase = 0;
             int dbg_i = 0;
             const unsigned base = smem_u32(smem);
-            for (int u = cta; u < n_units; u += ncta) {
-                const Unit w = unit_of(p, u);
-                const int kb_begin = w.g * p.kb_span;
-                const int nkb = min(p.kb_total, kb_begin + p.kb_span) - kb_begin;
+            bool first = true;
+            for_each_seg(p, cta, ncta, [&](const Seg& w) {
+                const int nkb = w.kb1 - w.kb0;
                 mbar_wait(acc_empty + acc, acc_phase ^ 1u);
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                 const unsigned d_tmem = tmem_base + unsigned(acc * p.bn);
@@ -274,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (lane == 0) probe_kb(p, dbg_i, 2);
                     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                     if (elect_one()) {
-                        if (i == 0 && u == cta) probe(p, 3);
+                        if (i == 0 && first) probe(p, 3);
                         const unsigned sa = base + unsigned(stage) * stage_bytes;
                         const unsigned sb = sa + p.a_tile_bytes;
 #pragma unroll
@@ -297,69 +346,41 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 if (elect_one()) {
-                    if (u == cta) probe(p, 4);
+                    if (first) probe(p, 4);
                     if constexpr (PAIR) umma_commit_pair(acc_full + acc);
                     else umma_commit(acc_full + acc);
                 }
+                first = false;
                 __syncwarp();
                 if (++acc == p.nacc) {
                     acc = 0;
                     acc_phase ^= 1u;
                 }
-            }
+            });
         }
     } else {
         // ---------------- epilogue (warps 2..5) ----------------
         const int quarter = warp & 3;  // TMEM lane quarter this warp may access
         const std::int64_t MN = std::int64_t(p.M) * p.N;
-        const std::int64_t tiles = std::int64_t(p.tiles_m) * p.tiles_n * (PAIR ? 2 : 1);
         const int chunk = p.bn >= 32 ? 32 : 16;
         const unsigned acc_empty_leader0 = PAIR ? mapa_shared(smem_u32(acc_empty), 0) : smem_u32(acc_empty);
+        const bool vec_ok = ((MN & 3) == 0) && ((reinterpret_cast<std::uintptr_t>(p.C) & 15) == 0) && ((p.N & 3) == 0);
+        __shared__ int s_last;
         int acc = 0;
         unsigned acc_phase = 0;
-        for (int u = cta; u < n_units; u += ncta) {
-            const Unit w = unit_of(p, u);
-            const bool last = (w.g == p.nz - 1);
+        bool first = true;
+        for_each_seg(p, cta, ncta, [&](const Seg& w) {
             // accumulator row -> TMEM lane: M = 128 (and each CTA of a pair):
             // row r in lane r; M = 64: rows 16q..16q+15 in lanes 32q..32q+15
             // of warp quarter q (the upper 16 lanes of each quarter unused)
             const int row = p.bm == 64 ? w.m0 + quarter * 16 + lane : w.m0 + int(rank) * 128 + quarter * 32 + lane;
             const bool row_ok = row < p.M && (p.bm == 64 ? lane < 16 : true);
-            // split-K flags are per CTA-half of a pair tile
-            const std::int64_t ftile = PAIR ? (std::int64_t(w.tile / p.tiles_n) * 2 + rank) * p.tiles_n +
-                                                  w.tile % p.tiles_n
-                                            : std::int64_t(w.tile);
+            const bool split = w.S > 1;
             mbar_wait(acc_full + acc, acc_phase);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            if (threadIdx.x == 64 && u == cta) probe(p, 5);
-            if (threadIdx.x == 64 && p.dbg != nullptr) {
-                unsigned long long t;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-                p.dbg[1024 + blockIdx.x * 4 + 1] = (long long)t;
-            }
-            if (last && p.nz > 1) {
-                for (int gg = threadIdx.x - 64; gg < p.nz - 1; gg += 128) {
-                    unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + ftile;
-                    unsigned long long v;
-                    while (true) {
-                        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(flag) : "memory");
-                        if (v == p.token) {
-                            // consumed: clear it, so a re-launch with the same token
-                            // (a replayed CUDA graph) waits for its own publication
-                            asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(0ull) : "memory");
-                            break;
-                        }
-                        __nanosleep(32);
-                    }
-                }
-                asm volatile("bar.sync 1, 128;\n" ::: "memory");
-                if (threadIdx.x == 64 && u == cta) probe(p, 6);
-                if (threadIdx.x == 64 && p.dbg != nullptr) {
-                    unsigned long long t;
-                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-                    p.dbg[1024 + blockIdx.x * 4 + 2] = (long long)t;
-                }
-            }
+            if (threadIdx.x == 64 && first) probe(p, 5);
+            // a split tile's segment goes to its partial slot j, else straight to C
+            float* out = split ? p.ws + std::int64_t(w.j) * MN : p.C;
             for (int c0 = 0; c0 < p.bn; c0 += chunk) {
                 float v[32];
                 const unsigned taddr = tmem_base + (unsigned(quarter * 32) << 16) + unsigned(acc * p.bn + c0);
@@ -375,94 +396,98 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const std::int64_t base = std::int64_t(row) * p.N + w.n0 + c0;
                 const int ncols = min(chunk, p.N - (w.n0 + c0));
                 if (ncols <= 0) continue;
-                const bool vec = ncols == chunk && ((base & 3) == 0) && ((MN & 3) == 0) &&
-                                 ((reinterpret_cast<std::uintptr_t>(p.C) & 15) == 0);
-                if (p.nz == 1 || last) {
-                    if (p.nz > 1) {
-                        // ordered fold of the published partials; every partial of
-                        // one slice is loaded before any add (one L2 round trip per slice)
-                        // Slices are folded in batches whose loads are all in
-                        // flight together (then added in slice order): 8 slices of
-                        // a 16-column chunk or 4 of a 32-column one per batch, so
-                        // a deep split (ICA: k_g = 32) costs a few L2 round trips.
-                        float accv[32];
+                float* dst = out + base;
+                if (ncols == chunk && vec_ok) {
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) accv[i] = 0.f;
-                        auto fold = [&]<int CH, int FB>() {
-                            for (int g0 = 0; g0 < p.nz - 1; g0 += FB) {
-                                float part[FB][CH];
-#pragma unroll
-                                for (int f = 0; f < FB; ++f) {
-                                    const bool live = g0 + f < p.nz - 1;
-                                    const float* src = p.ws + (g0 + f) * MN + base;
-                                    if (vec) {
-#pragma unroll
-                                        for (int i = 0; i < CH; i += 4) {
-                                            if (live) {
-                                                const float4 q = __ldcg(reinterpret_cast<const float4*>(src + i));
-                                                part[f][i] = q.x;
-                                                part[f][i + 1] = q.y;
-                                                part[f][i + 2] = q.z;
-                                                part[f][i + 3] = q.w;
-                                            } else {
-                                                part[f][i] = part[f][i + 1] = part[f][i + 2] = part[f][i + 3] = 0.f;
-                                            }
-                                        }
-                                    } else {
-#pragma unroll
-                                        for (int i = 0; i < CH; ++i)
-                                            part[f][i] = (live && i < ncols) ? __ldcg(src + i) : 0.f;
-                                    }
-                                }
-#pragma unroll
-                                for (int f = 0; f < FB; ++f)
-                                    if (g0 + f < p.nz - 1)
-#pragma unroll
-                                        for (int i = 0; i < CH; ++i) accv[i] = __fadd_rn(accv[i], part[f][i]);
-                            }
-                        };
-                        if (chunk == 16) fold.template operator()<16, 8>();
-                        else fold.template operator()<32, 4>();
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) v[i] = __fadd_rn(accv[i], v[i]);
-                    }
-                    float* dst = p.C + base;
-                    if (vec) {
-#pragma unroll
-                        for (int i = 0; i < 32; i += 4)
-                            if (i < chunk)
-                                *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                    } else {
-                        for (int i = 0; i < ncols; ++i) dst[i] = v[i];
-                    }
+                    for (int i = 0; i < 32; i += 4)
+                        if (i < chunk) {
+                            if (split) __stcg(reinterpret_cast<float4*>(dst + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+                            else *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                        }
                 } else {
-                    float* dst = p.ws + std::int64_t(w.g) * MN + base;
-                    if (vec) {
-#pragma unroll
-                        for (int i = 0; i < 32; i += 4)
-                            if (i < chunk)
-                                __stcg(reinterpret_cast<float4*>(dst + i),
-                                       make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
-                    } else {
-                        for (int i = 0; i < ncols; ++i) __stcg(dst + i, v[i]);
+                    for (int i = 0; i < ncols; ++i) {
+                        if (split) __stcg(dst + i, v[i]);
+                        else dst[i] = v[i];
                     }
-                }
-            }
-            if (!last && p.nz > 1) {
-                // bar.sync orders the 128 threads' partial stores before one
-                // thread's cumulative gpu-scope release (no per-thread fence)
-                asm volatile("bar.sync 1, 128;\n" ::: "memory");
-                if (threadIdx.x == 64) {
-                    unsigned long long* flag = p.flags + std::int64_t(w.g) * tiles + ftile;
-                    asm volatile("fence.acq_rel.gpu;\nst.release.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(p.token)
-                                 : "memory");
                 }
             }
             if (++acc == p.nacc) {
                 acc = 0;
                 acc_phase ^= 1u;
             }
-        }
+            first = false;
+            if (!split) return;
+            // ---- two-level fold of the tile's segments (no waiting) -------
+            const int ngroups = (w.S + kFoldGroup - 1) / kFoldGroup;
+            const int q = w.j / kFoldGroup;
+            const int g_lo = q * kFoldGroup, g_hi = min(w.S, g_lo + kFoldGroup);
+            const std::int64_t ctile = (PAIR ? std::int64_t(w.tile) * 2 + rank : std::int64_t(w.tile)) * (p.gmax + 1);
+            unsigned* ctr_group = p.counters + ctile + q;
+            unsigned* ctr_tile = p.counters + ctile + p.gmax;
+            // fold slots [lo, hi) of `src` (stride MN) in order into `dstbuf` (this thread's row)
+            auto fold = [&](const float* src, int lo, int hi, float* dstbuf, bool to_c) {
+                if (!row_ok) return;
+                for (int c0 = 0; c0 < p.bn; c0 += 16) {
+                    const std::int64_t base = std::int64_t(row) * p.N + w.n0 + c0;
+                    const int ncols = min(16, p.N - (w.n0 + c0));
+                    if (ncols <= 0) break;
+                    float accv[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) accv[i] = 0.f;
+                    for (int g0 = lo; g0 < hi; g0 += 8) {
+                        float part[8][16];
+#pragma unroll
+                        for (int f = 0; f < 8; ++f) {
+                            const float* sp = src + std::int64_t(g0 + f) * MN + base;
+                            const bool live = g0 + f < hi;
+                            if (ncols == 16 && vec_ok) {
+#pragma unroll
+                                for (int i = 0; i < 16; i += 4) {
+                                    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+                                    if (live) x = __ldcg(reinterpret_cast<const float4*>(sp + i));
+                                    part[f][i] = x.x; part[f][i + 1] = x.y; part[f][i + 2] = x.z; part[f][i + 3] = x.w;
+                                }
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) part[f][i] = (live && i < ncols) ? __ldcg(sp + i) : 0.f;
+                            }
+                        }
+#pragma unroll
+                        for (int f = 0; f < 8; ++f)
+                            if (g0 + f < hi)
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) accv[i] = __fadd_rn(accv[i], part[f][i]);
+                    }
+                    float* dp = dstbuf + base;
+                    for (int i = 0; i < ncols; ++i) {
+                        if (to_c) dp[i] = accv[i];
+                        else __stcg(dp + i, accv[i]);
+                    }
+                }
+            };
+            // arrival: bar.sync orders the 128 threads' stores before one
+            // thread's cumulative gpu-scope release (acq_rel atomic)
+            auto arrive_last = [&](unsigned* ctr, int expected) {
+                asm volatile("bar.sync 1, 128;\n" ::: "memory");
+                if (threadIdx.x == 64) {
+                    unsigned prev;
+                    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;\n" : "=r"(prev) : "l"(ctr) : "memory");
+                    const int last = int(prev) + 1 == expected;
+                    if (last) asm volatile("st.relaxed.gpu.global.u32 [%0], 0;\n" ::"l"(ctr) : "memory");
+                    s_last = last;
+                }
+                asm volatile("bar.sync 1, 128;\n" ::: "memory");
+                return s_last != 0;
+            };
+            if (!arrive_last(ctr_group, g_hi - g_lo)) return;
+            if (ngroups == 1) {
+                fold(p.ws, 0, w.S, p.C, true);
+                return;
+            }
+            fold(p.ws, g_lo, g_hi, p.ws2 + std::int64_t(q) * MN, false);
+            if (!arrive_last(ctr_tile, ngroups)) return;
+            fold(p.ws2, 0, ngroups, p.C, true);
+        });
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     if constexpr (PAIR) cluster_sync();  // the peer's MMAs / smem reads are done before either CTA frees
@@ -498,7 +523,7 @@ struct TcPlan {
     TcParams p{};
     dim3 grid;
     std::size_t smem{0};
-    std::size_t ws_bytes{0}, flag_bytes{0};
+    std::size_t ws_bytes{0};
     int kind{0};
     int ksteps{4};
     bool pair{false};  // m_l = 256: cluster of two CTAs, tcgen05.mma.cta_group::2
@@ -575,8 +600,6 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     if ((a_ld * es) % 16 != 0 || (b_ld * es) % 16 != 0)
         throw unsupported_error("tensor-core family: leading dimensions must be multiples of 16 bytes for TMA");
     p.kb_total = int(ceil_div(in.k, p.bk));
-    p.kb_span = int(ceil_div(p.kb_total, t.k_g));
-    p.nz = int(ceil_div(p.kb_total, p.kb_span));
     const std::size_t stage_bytes = std::size_t(p.a_tile_bytes) + p.b_tile_bytes;
     const std::size_t extra = 1024 + 8 * 32 + 64;  // alignment slack + barriers (2*stages + 4) + tmem slot
     const std::size_t optin = std::size_t(smem_optin());
@@ -618,22 +641,35 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
         p.b_koff[kk] = p.b_kmajor ? (kb / p.b_sw) * p.b_box_stride + kb % p.b_sw : (kb / es) * p.b_sw;
     }
     pl.ksteps = ksteps;
-    // persistent grid: one CTA per SM (shared memory holds one CTA), static
-    // round-robin over (tile, slice) units
-    const std::int64_t units = std::int64_t(p.tiles_m) * p.tiles_n * p.nz;
-    if (units > 0x7fffffff) throw unsupported_error("too many work units for one launch");
-    if (pl.pair) {
-        // one CTA per SM, two per cluster: at most (SMs / 2) co-resident pairs
-        pl.grid = dim3(unsigned(2 * std::min<std::int64_t>(units, num_sms() / 2)), 1, 1);
-    } else {
-        // one CTA per SM: the epilogue's batched split-K fold needs ~240
-        // registers per thread, so two 192-thread CTAs never co-reside
-        pl.grid = dim3(unsigned(std::min<std::int64_t>(units, num_sms())), 1, 1);
+    // persistent grid: one CTA (or CTA pair) per SM (shared memory holds
+    // one CTA).  k_g = 1: whole tiles round-robin.  k_g > 1: stream-K --
+    // min(SMs, tiles * k_g) CTAs each take an equal contiguous share of the
+    // (tile, k-block) iterations, so every SM streams the same k-blocks
+    const std::int64_t tiles = std::int64_t(p.tiles_m) * p.tiles_n;
+    if (tiles > 0x7fffffff) throw unsupported_error("too many output tiles for one launch");
+    const std::int64_t slots = pl.pair ? num_sms() / 2 : num_sms();
+    p.streamk = t.k_g > 1 ? 1 : 0;
+    p.total_it = tiles * p.kb_total;
+    std::int64_t G = p.streamk ? std::min<std::int64_t>({slots, tiles * t.k_g, p.total_it})
+                               : std::min<std::int64_t>(slots, tiles);
+    G = std::max<std::int64_t>(G, 1);
+    pl.grid = dim3(unsigned(pl.pair ? 2 * G : G), 1, 1);
+    p.smax = 1;
+    if (p.streamk) {
+        auto cfind = [&](std::int64_t i) { return ((i + 1) * G - 1) / p.total_it; };
+        for (std::int64_t tl = 0; tl < tiles; ++tl) {
+            const std::int64_t S = cfind((tl + 1) * p.kb_total - 1) - cfind(tl * p.kb_total) + 1;
+            p.smax = int(std::max<std::int64_t>(p.smax, S));
+        }
     }
-    if (p.nz > 1) {
-        pl.flag_bytes = (std::size_t(p.tiles_m) * (pl.pair ? 2 : 1) * p.tiles_n * std::size_t(p.nz - 1) * 8 + 255) /
-                        256 * 256;
-        pl.ws_bytes = dev::kSplitCounterBytes + pl.flag_bytes + std::size_t(p.nz - 1) * std::size_t(in.m) * std::size_t(in.n) * 4;
+    p.gmax = (p.smax + ktune_dev::tc::kFoldGroup - 1) / ktune_dev::tc::kFoldGroup;
+    if (p.smax > 1) {
+        const std::size_t ctr = std::size_t(tiles) * (pl.pair ? 2 : 1) * std::size_t(p.gmax + 1) * sizeof(unsigned);
+        if (ctr > dev::kSplitCounterBytes)
+            throw unsupported_error("tensor-core family: stream-K over " + std::to_string(tiles) +
+                                    " tiles exceeds the split-K counter region");
+        pl.ws_bytes = dev::kSplitCounterBytes +
+                      std::size_t(p.smax + p.gmax) * std::size_t(in.m) * std::size_t(in.n) * sizeof(float);
     }
     return pl;
 }
@@ -657,14 +693,15 @@ void gemm(const GemmInput& in, const GemmTuning& t, const void* a, const void* b
         throw unsupported_error("tensor-core family: operand pointers must be 16-byte aligned for TMA");
     p.C = static_cast<float*>(c);
     if (const char* d = std::getenv("KTUNE_TC_DEBUG")) p.dbg = reinterpret_cast<long long*>(std::strtoull(d, nullptr, 0));
-    if (p.nz > 1) {
+    if (p.smax > 1) {
         if (ws == nullptr || ws_bytes < pl.ws_bytes)
             throw workspace_error("workspace of " + std::to_string(ws_bytes) + " bytes is smaller than the " +
                                   std::to_string(pl.ws_bytes) + " bytes this tuning needs");
-        // past the SIMT family's zeroed counter region (kernels.hpp)
-        p.flags = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(ws) + dev::kSplitCounterBytes);
-        p.ws = reinterpret_cast<float*>(static_cast<unsigned char*>(ws) + dev::kSplitCounterBytes + pl.flag_bytes);
-        p.token = next_token();
+        // arrival counters in the zeroed counter region (kernels.hpp), then
+        // the segment and fold-group partials
+        p.counters = static_cast<unsigned*>(ws);
+        p.ws = reinterpret_cast<float*>(static_cast<unsigned char*>(ws) + dev::kSplitCounterBytes);
+        p.ws2 = p.ws + std::size_t(p.smax) * std::size_t(in.m) * std::size_t(in.n);
     }
     const int es = p.esize;
     // A: K-major -> [M][K] rows, boxes {a_sw/es along K, bm}; MN-major -> [K][M], boxes {a_sw/es along M, bk}
