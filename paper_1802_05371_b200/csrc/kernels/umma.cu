@@ -56,6 +56,7 @@ struct TcParams {
     int a_kmajor, b_kmajor;
     int a_sw, b_sw;               // swizzle span (bytes) of each operand's tiles
     int a_boxes, b_boxes;         // TMA boxes per stage
+    int a_rows, b_rows;           // rows per K-major box actually streamed (<= bm / bn per CTA)
     unsigned a_box_bytes, b_box_bytes;
     unsigned a_tile_bytes, b_tile_bytes;  // per stage, 1024-aligned
     unsigned a_box_stride, b_box_stride;  // smem distance between boxes of one stage
@@ -77,7 +78,14 @@ struct TcParams {
 };
 
 
-constexpr int kThreads = 192;
+// warps 0..kProducers-1: TMA producers (a TMA issue occupies its warp for a
+// few hundred cycles, so the boxes of a stage are dealt round-robin over
+// several warps: measured per-SM ingest scales with the issuing warps);
+// warp kProducers: MMA issuer; warps 4..7: epilogue (TMEM lane quarters 0..3)
+constexpr int kProducers = 3;
+constexpr int kMmaWarp = 3;
+constexpr int kEpi0 = 128;  // first epilogue thread
+constexpr int kThreads = 256;
 
 // Debug timeline (KTUNE_TC_DEBUG=<device pointer>): %globaltimer of events of
 // the CTAs with blockIdx.x = blockIdx.y = 0, 8 slots per grid slice.
@@ -208,18 +216,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
-            mbar_init(full + s, 1);  // pair: the leader's arrive.expect_tx covers both CTAs' bytes
+            // one arrive.expect_tx per producer warp (pair: the leader's
+            // producers expect both CTAs' bytes of their boxes)
+            mbar_init(full + s, kProducers);
             mbar_init(empty + s, 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(acc_full + a, 1);
-            mbar_init(acc_empty + a, PAIR ? 256 : 128);
+            mbar_init(acc_empty + a, PAIR ? 256 : 128);  // every epilogue thread of the CTA (pair)
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&tma_a)) : "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&tma_b)) : "memory");
     }
-    if (warp == 1) {
+    if (warp == kMmaWarp) {
         if constexpr (PAIR) {
             asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                              smem_u32(tmem_slot)),
@@ -240,12 +250,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) probe(p, 1);
     pdl_wait();  // setup above overlaps the previous kernel; global work starts here
 
-    if (warp == 0) {
-        // ---------------- TMA producer (whole warp loops, one lane issues) ----------------
+    if (warp < kProducers) {
+        // ---------------- TMA producers (each warp loops, one lane issues) ----------------
+        // Box b of a stage (A boxes first, then B boxes) is issued by warp
+        // b % kProducers; every producer arrives on the stage's full barrier
+        // with the bytes of its own boxes (x2 for a pair: the follower issues
+        // the same boxes onto the leader's barrier).
         int stage = 0;
         unsigned phase = 0;
         const int a_box_elems = p.a_sw / p.esize, b_box_elems = p.b_sw / p.esize;
-        const unsigned tx_bytes = p.a_boxes * p.a_box_bytes + p.b_boxes * p.b_box_bytes;
+        const int nbox = p.a_boxes + p.b_boxes;
+        unsigned my_bytes = 0;
+        for (int b = warp; b < nbox; b += kProducers) my_bytes += b < p.a_boxes ? p.a_box_bytes : p.b_box_bytes;
         const int a_row = PAIR ? int(rank) * 128 : 0;                 // this CTA's rows of the tile
         const int b_col = PAIR ? int(rank) * (p.bn / 2) : 0;          // this CTA's half of the columns
         int dbg_i = 0;
@@ -253,9 +269,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for_each_seg(p, cta, ncta, [&](const Seg& w) {
             for (int kb = w.kb0; kb < w.kb1; ++kb, ++dbg_i) {
                 mbar_wait(empty + stage, phase ^ 1u);
-                if (lane == 0) probe_kb(p, dbg_i, 0);
+                if (lane == 0 && warp == 0) probe_kb(p, dbg_i, 0);
                 if (elect_one()) {
-                    if (first) probe(p, 2);
+                    if (first && warp == 0) probe(p, 2);
                     first = false;
                     unsigned char* sa = smem + std::size_t(stage) * stage_bytes;
                     unsigned char* sb = sa + p.a_tile_bytes;
@@ -264,30 +280,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if constexpr (PAIR) {
                         const unsigned bar = mapa_shared(smem_u32(full + stage), 0);  // the leader's
                         // the follower's bytes may land before the leader's expect_tx:
-                        // the phase cannot complete until the leader (count 1) arrives
-                        if (leader) mbar_expect_tx(full + stage, 2 * tx_bytes);
-                        for (int j = 0; j < p.a_boxes; ++j) {
-                            if (p.a_kmajor) tma_load_2d_pair(sa + j * p.a_box_stride, &tma_a, bar, k0 + j * a_box_elems, m0);
-                            else tma_load_2d_pair(sa + j * p.a_box_stride, &tma_a, bar, m0 + j * a_box_elems, k0);
+                        // the phase cannot complete until the leader's producers arrive
+                        if (leader) mbar_expect_tx(full + stage, 2 * my_bytes);
+                        for (int b = warp; b < nbox; b += kProducers) {
+                            if (b < p.a_boxes) {
+                                const int j = b;
+                                if (p.a_kmajor) tma_load_2d_pair(sa + j * p.a_box_stride, &tma_a, bar, k0 + j * a_box_elems, m0);
+                                else tma_load_2d_pair(sa + j * p.a_box_stride, &tma_a, bar, m0 + j * a_box_elems, k0);
+                            } else {
+                                const int j = b - p.a_boxes;
+                                if (p.b_kmajor) tma_load_2d_pair(sb + j * p.b_box_stride, &tma_b, bar, k0 + j * b_box_elems, n0);
+                                else tma_load_2d_pair(sb + j * p.b_box_stride, &tma_b, bar, n0 + j * b_box_elems, k0);
+                            }
                         }
-                        for (int j = 0; j < p.b_boxes; ++j) {
-                            if (p.b_kmajor) tma_load_2d_pair(sb + j * p.b_box_stride, &tma_b, bar, k0 + j * b_box_elems, n0);
-                            else tma_load_2d_pair(sb + j * p.b_box_stride, &tma_b, bar, n0 + j * b_box_elems, k0);
-                        }
-                        probe_kb(p, dbg_i, 1);
+                        if (warp == 0) probe_kb(p, dbg_i, 1);
                     } else {
-                        mbar_expect_tx(full + stage, tx_bytes);
-                        for (int j = 0; j < p.a_boxes; ++j) {
-                            if (p.a_kmajor)
-                                tma_load_2d(sa + j * p.a_box_stride, &tma_a, full + stage, k0 + j * a_box_elems, m0);
-                            else
-                                tma_load_2d(sa + j * p.a_box_stride, &tma_a, full + stage, m0 + j * a_box_elems, k0);
-                        }
-                        for (int j = 0; j < p.b_boxes; ++j) {
-                            if (p.b_kmajor)
-                                tma_load_2d(sb + j * p.b_box_stride, &tma_b, full + stage, k0 + j * b_box_elems, n0);
-                            else
-                                tma_load_2d(sb + j * p.b_box_stride, &tma_b, full + stage, n0 + j * b_box_elems, k0);
+                        mbar_expect_tx(full + stage, my_bytes);
+                        for (int b = warp; b < nbox; b += kProducers) {
+                            if (b < p.a_boxes) {
+                                const int j = b;
+                                if (p.a_kmajor)
+                                    tma_load_2d(sa + j * p.a_box_stride, &tma_a, full + stage, k0 + j * a_box_elems, m0);
+                                else
+                                    tma_load_2d(sa + j * p.a_box_stride, &tma_a, full + stage, m0 + j * a_box_elems, k0);
+                            } else {
+                                const int j = b - p.a_boxes;
+                                if (p.b_kmajor)
+                                    tma_load_2d(sb + j * p.b_box_stride, &tma_b, full + stage, k0 + j * b_box_elems, n0);
+                                else
+                                    tma_load_2d(sb + j * p.b_box_stride, &tma_b, full + stage, n0 + j * b_box_elems, k0);
+                            }
                         }
                     }
                 }
@@ -298,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         });
-    } else if (warp == 1) {
+    } else if (warp == kMmaWarp) {
         // ---------------- MMA issuer (whole warp loops, one lane issues) ----------------
         // Descriptors: constant high words and k-slice offsets come from the
         // host; per k-block only the 14-bit start address changes.  With
@@ -359,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             });
         }
     } else {
-        // ---------------- epilogue (warps 2..5) ----------------
+        // ---------------- epilogue (warps 4..7) ----------------
         const int quarter = warp & 3;  // TMEM lane quarter this warp may access
         const std::int64_t MN = std::int64_t(p.M) * p.N;
         const int chunk = p.bn >= 32 ? 32 : 16;
@@ -378,7 +400,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool split = w.S > 1;
             mbar_wait(acc_full + acc, acc_phase);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            if (threadIdx.x == 64 && first) probe(p, 5);
+            if (threadIdx.x == kEpi0 && first) probe(p, 5);
+            if (threadIdx.x == kEpi0 && p.dbg != nullptr) {  // per-CTA: accumulator ready (last segment)
+                unsigned long long tt;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+                p.dbg[1024 + blockIdx.x * 4 + 1] = (long long)tt;
+            }
             // a split tile's segment goes to its partial slot j, else straight to C
             float* out = split ? p.ws + std::int64_t(w.j) * MN : p.C;
             for (int c0 = 0; c0 < p.bn; c0 += chunk) {
@@ -469,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // thread's cumulative gpu-scope release (acq_rel atomic)
             auto arrive_last = [&](unsigned* ctr, int expected) {
                 asm volatile("bar.sync 1, 128;\n" ::: "memory");
-                if (threadIdx.x == 64) {
+                if (threadIdx.x == kEpi0) {
                     unsigned prev;
                     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;\n" : "=r"(prev) : "l"(ctr) : "memory");
                     const int last = int(prev) + 1 == expected;
@@ -479,7 +506,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 asm volatile("bar.sync 1, 128;\n" ::: "memory");
                 return s_last != 0;
             };
-            if (!arrive_last(ctr_group, g_hi - g_lo)) return;
+            const bool last_in_group = arrive_last(ctr_group, g_hi - g_lo);
+            if (threadIdx.x == kEpi0 && p.dbg != nullptr) {  // per-CTA: ticket taken
+                unsigned long long tt;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+                p.dbg[1024 + blockIdx.x * 4 + 2] = (long long)tt;
+            }
+            if (!last_in_group) return;
             if (ngroups == 1) {
                 fold(p.ws, 0, w.S, p.C, true);
                 return;
@@ -498,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.dbg[1024 + blockIdx.x * 4 + 3] = (long long)t;
     }
-    if (warp == 1) {
+    if (warp == kMmaWarp) {
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         if constexpr (PAIR)
             asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(p.tmem_cols));
@@ -593,8 +626,24 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     }
     p.a_box_stride = p.a_box_bytes;
     p.b_box_stride = p.b_box_bytes;
-    p.a_tile_bytes = unsigned(ceil_div(std::int64_t(p.a_boxes) * p.a_box_bytes, 1024) * 1024);
-    p.b_tile_bytes = unsigned(ceil_div(std::int64_t(p.b_boxes) * p.b_box_bytes, 1024) * 1024);
+    // A single row tile taller than the matrix (M < m_l, e.g. ICA's 32 rows
+    // in a 64-row UMMA tile): stream only the rows that exist.  TMA costs a
+    // few cycles per box row whatever its width, and rows past M only feed
+    // accumulator rows that are never stored (each D row depends on its own
+    // A row), so the stale shared memory there is harmless.  Same for the
+    // columns of a K-major B narrower than n_l.
+    p.a_rows = p.bm;
+    p.b_rows = bn_cta;
+    if (p.a_kmajor && !pl.pair && in.m < p.bm) {
+        p.a_rows = int(std::min<std::int64_t>(p.bm, ceil_div(in.m, 8) * 8));
+        p.a_box_bytes = unsigned(p.a_sw) * unsigned(p.a_rows);
+    }
+    if (p.b_kmajor && !pl.pair && in.n < bn_cta) {
+        p.b_rows = int(std::min<std::int64_t>(bn_cta, ceil_div(in.n, 8) * 8));
+        p.b_box_bytes = unsigned(p.b_sw) * unsigned(p.b_rows);
+    }
+    p.a_tile_bytes = unsigned(ceil_div(std::int64_t(p.a_boxes) * p.a_box_stride, 1024) * 1024);
+    p.b_tile_bytes = unsigned(ceil_div(std::int64_t(p.b_boxes) * p.b_box_stride, 1024) * 1024);
     // TMA: global strides must be multiples of 16 bytes
     const std::int64_t a_ld = in.trans_a ? in.m : in.k, b_ld = in.trans_b ? in.k : in.n;
     if ((a_ld * es) % 16 != 0 || (b_ld * es) % 16 != 0)
@@ -705,9 +754,9 @@ void gemm(const GemmInput& in, const GemmTuning& t, const void* a, const void* b
     }
     const int es = p.esize;
     // A: K-major -> [M][K] rows, boxes {a_sw/es along K, bm}; MN-major -> [K][M], boxes {a_sw/es along M, bk}
-    CUtensorMap ma = p.a_kmajor ? make_map(a, in.dtype, in.k, in.m, p.a_sw / es, p.bm, p.a_sw)
+    CUtensorMap ma = p.a_kmajor ? make_map(a, in.dtype, in.k, in.m, p.a_sw / es, p.a_rows, p.a_sw)
                                 : make_map(a, in.dtype, in.m, in.k, p.a_sw / es, p.bk, p.a_sw);
-    CUtensorMap mb = p.b_kmajor ? make_map(b, in.dtype, in.k, in.n, p.b_sw / es, pl.pair ? p.bn / 2 : p.bn, p.b_sw)
+    CUtensorMap mb = p.b_kmajor ? make_map(b, in.dtype, in.k, in.n, p.b_sw / es, p.b_rows, p.b_sw)
                                 : make_map(b, in.dtype, in.n, in.k, p.b_sw / es, p.bk, p.b_sw);
     using ktune_dev::tc::umma_gemm_kernel;
 #define KTUNE_TC_ROW(K, P)                                                                           \
