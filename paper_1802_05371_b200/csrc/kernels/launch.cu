@@ -462,7 +462,20 @@ TmaLaunch tma_geometry(const GemmInput& in, const Plan& pl, Mode mode, const voi
     g.neg_zero = 0x80000000u;
     g.compute_only = std::getenv("KTUNE_SIMT_COMPUTE_ONLY") != nullptr ? 1 : 0;
     g.producer_warp = (pl.threads + 31) / 32;
-    tl.threads = g.producer_warp * 32 + 32;
+    // a TMA issue keeps its warp busy for a few hundred cycles: up to 4
+    // producer warps share a step's boxes (KTUNE_SIMT_PRODUCERS overrides)
+    // when a block has the SM (nearly) to itself; with several resident
+    // blocks per SM their own producers already overlap, and the extra
+    // warps' registers were measured to cost more than they bring
+    // (bench protocol, 2560x16x2560: P = 1 best at 4-5 blocks per SM)
+    const int boxes_per_step = p.kl * (g.a_nbox + g.b_nbox);
+    {
+        const std::int64_t blocks_total = std::int64_t(pl.col_tiles) * pl.row_tiles * p.nz;
+        const std::int64_t per_sm = std::max<std::int64_t>(1, ceil_div(blocks_total, device_sm_count()));
+        g.n_producers = per_sm <= 2 ? std::clamp(boxes_per_step, 1, 4) : 1;
+    }
+    if (const char* e = std::getenv("KTUNE_SIMT_PRODUCERS")) g.n_producers = std::clamp(std::atoi(e), 1, 4);
+    tl.threads = (g.producer_warp + g.n_producers) * 32;
     // pipeline depth: as deep as shared memory allows while the whole grid
     // stays resident in one wave (per-block footprint = dynamic smem + the
     // 1 KB the hardware reserves per block); TMA needs no register budget

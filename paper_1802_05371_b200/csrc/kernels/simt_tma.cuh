@@ -38,7 +38,8 @@ struct TmaGeom {
     int a_grp, b_grp;    // bytes of one group's A / B region in a stage
     int stage_bytes;     // kl * (a_grp + b_grp)
     int compute_threads; // tm*tn*kl
-    int producer_warp;   // warp index of the TMA producer
+    int producer_warp;   // warp index of the first TMA producer
+    int n_producers;     // TMA producer warps (boxes dealt round-robin: a TMA issue occupies its warp)
     unsigned neg_zero;   // 0x80000000 (-0.0f), opaque to ptxas (see mac2)
     int compute_only;    // measurement aid (KTUNE_SIMT_COMPUTE_ONLY): no TMA, no stage waits -- wrong results
 };
@@ -129,7 +130,7 @@ __device__ __forceinline__ void tma_prefetch_map(const CUtensorMap* map) {
 __device__ __forceinline__ int swz_row_xor(int row, int rb) { return ((row * rb) >> 3) & (rb - 16); }
 
 template <typename T, int MS_, int NS_, int KS_, bool PARITY, bool ARM, bool BRM, bool NARROW>
-__global__ void __launch_bounds__(NARROW ? kNarrowThreads + 32 : 1024)
+__global__ void __launch_bounds__(NARROW ? kNarrowThreads + 4 * 32 : 1024)
     simt_tma_kernel(const __grid_constant__ CUtensorMap a_map, const __grid_constant__ CUtensorMap b_map,
                     const GemmProblem<T> prob, const SimtParams p, const TmaGeom g) {
     static_assert(MS_ > 0, "register-tile instantiations only");
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 32 : 1024)
 
     if (tid == 0) {
         for (int s = 0; s < p.stages; ++s) {
-            tma_mbar_init(&full[s], 1);
+            tma_mbar_init(&full[s], unsigned(g.n_producers));
             tma_mbar_init(&empty[s], unsigned(compute_warps));
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -206,12 +207,16 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 32 : 1024)
     const int my_lo = min(s_hi, s_lo + lg * kl_span);
     const int my_hi = min(s_hi, my_lo + kl_span);
 
-    if (warp == g.producer_warp && !g.compute_only) {
-        // ---- TMA producer (one lane) ------------------------------------
+    if (warp >= g.producer_warp && !g.compute_only) {
+        // ---- TMA producers (one lane each) ------------------------------
+        // The boxes of a step -- per live group: A boxes then B boxes -- are
+        // dealt round-robin over the producer warps; each arrives on the
+        // stage's full barrier with the bytes of its own boxes.
+        const int pw = warp - g.producer_warp;
         if (lane == 0) {
             int slot = 0;
             unsigned phase = 0;  // parity of the ring pass (stage reuse count & 1)
-            const unsigned group_bytes = unsigned(g.a_nbox * g.a_box_bytes + g.b_nbox * g.b_box_bytes);
+            const int per_group = g.a_nbox + g.b_nbox;
             // groups still streaming at step st: those with len(gx) > st*w;
             // lengths are non-increasing in gx (only the last groups run short)
             for (int st = 0; st < nsteps; ++st) {
@@ -223,18 +228,22 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 32 : 1024)
                     const int ghi = min(s_hi, glo + kl_span);
                     live += (glo + off < ghi) ? 1 : 0;
                 }
-                tma_mbar_expect_tx(&full[slot], unsigned(live) * group_bytes);
+                unsigned mine = 0;
+                for (int b = pw; b < live * per_group; b += g.n_producers)
+                    mine += unsigned(b % per_group < g.a_nbox ? g.a_box_bytes : g.b_box_bytes);
+                tma_mbar_expect_tx(&full[slot], mine);
                 unsigned char* stage = stages_mem + slot * g.stage_bytes;
-                for (int gx = 0; gx < live; ++gx) {
+                for (int b = pw; b < live * per_group; b += g.n_producers) {
+                    const int gx = b / per_group, j = b - gx * per_group;
                     const int kc = min(s_hi, s_lo + gx * kl_span) + off;
                     unsigned char* ga = stage + gx * (g.a_grp + g.b_grp);
                     unsigned char* gb = ga + g.a_grp;
-                    for (int b = 0; b < g.a_nbox; ++b) {
-                        if constexpr (ARM) tma_box_2d(ga + b * g.a_box_stride, &a_map, &full[slot], int(kc) + b * g.a_wb, int(row0));
+                    if (j < g.a_nbox) {
+                        if constexpr (ARM) tma_box_2d(ga + j * g.a_box_stride, &a_map, &full[slot], int(kc) + j * g.a_wb, int(row0));
                         else tma_box_2d(ga, &a_map, &full[slot], int(row0), int(kc));
-                    }
-                    for (int b = 0; b < g.b_nbox; ++b) {
-                        if constexpr (BRM) tma_box_2d(gb + b * g.b_box_stride, &b_map, &full[slot], int(kc) + b * g.b_wb, col0);
+                    } else {
+                        const int jb = j - g.a_nbox;
+                        if constexpr (BRM) tma_box_2d(gb + jb * g.b_box_stride, &b_map, &full[slot], int(kc) + jb * g.b_wb, col0);
                         else tma_box_2d(gb, &b_map, &full[slot], col0, int(kc));
                     }
                 }
