@@ -321,6 +321,27 @@ KTUNE_API int ktune_infer_gemm(const ktune_hw* hw, const char* bounds_json, cons
 KTUNE_API int ktune_infer_conv(const ktune_hw* hw, const char* bounds_json, const char* model_json,
                                const ktune_conv_input* in, int32_t top_k, int32_t backend,
                                const ktune_measure_options* opts);
+/* Sharded top-k re-measure (pipeline.cpp:674-680; with
+ * top_k >= the legal space this is `bench --exhaustive`): every rank ranks
+ * the same candidates and measures positions i with i % world == rank;
+ * gflops_out[i] = the measurement, or -1 for another rank's position
+ * (*count = candidates ranked).  After an element-wise max over ranks,
+ * ktune_infer_*_replay rebuilds the ktune-result-1 JSON exactly as the
+ * sequential infer_* would (ktune_last_text()). */
+KTUNE_API int ktune_infer_gemm_shard(const ktune_hw* hw, const char* bounds_json, const char* model_json,
+                                     const ktune_gemm_input* in, int32_t top_k, int32_t backend,
+                                     const ktune_measure_options* opts, int32_t rank, int32_t world,
+                                     double* gflops_out, int64_t cap, int64_t* count);
+KTUNE_API int ktune_infer_conv_shard(const ktune_hw* hw, const char* bounds_json, const char* model_json,
+                                     const ktune_conv_input* in, int32_t top_k, int32_t backend,
+                                     const ktune_measure_options* opts, int32_t rank, int32_t world,
+                                     double* gflops_out, int64_t cap, int64_t* count);
+KTUNE_API int ktune_infer_gemm_replay(const ktune_hw* hw, const char* bounds_json, const char* model_json,
+                                      const ktune_gemm_input* in, int32_t top_k, const char* backend_name,
+                                      const double* gflops, int64_t n);
+KTUNE_API int ktune_infer_conv_replay(const ktune_hw* hw, const char* bounds_json, const char* model_json,
+                                      const ktune_conv_input* in, int32_t top_k, const char* backend_name,
+                                      const double* gflops, int64_t n);
 KTUNE_API int ktune_cache_key_gemm(const ktune_gemm_input* in);
 KTUNE_API int ktune_cache_key_conv(const ktune_conv_input* in);
 /* *found = 1 and the entry's JSON in ktune_last_text(), or *found = 0. */
@@ -332,6 +353,13 @@ KTUNE_API int ktune_cache_store(const char* dir, const char* result_json);
 KTUNE_API int ktune_select_gemm(const ktune_hw* hw, const char* bounds_json, const char* model_json,
                                 const char* cache_dir, const ktune_gemm_input* in, int32_t top_k,
                                 ktune_gemm_tuning* chosen, int32_t* source /* 0 memory, 1 file, 2 inferred */);
+
+/* Runtime pick for a convolution (infer_conv, pipeline.cpp:687-723, plus the
+ * result cache :936-997): in-memory map (keyed by the input signature, hw,
+ * bounds, model and top_k) -> result cache -> infer_conv on the b200 backend. */
+KTUNE_API int ktune_select_conv(const ktune_hw* hw, const char* bounds_json, const char* model_json,
+                                const char* cache_dir, const ktune_conv_input* in, int32_t top_k,
+                                ktune_conv_tuning* chosen, int32_t* source /* 0 memory, 1 file, 2 inferred */);
 
 /* ---- KTN1 tensor files (replaces proj/src/tensor_file.cpp:36-112) -----------
  * Same bytes as the reference writer: "KTN1", int32 element size, int32 rank,

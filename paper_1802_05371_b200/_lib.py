@@ -196,6 +196,18 @@ _SIGNATURES = {
     "ktune_cache_lookup_gemm": ([ctypes.c_char_p, _P(GemmInputC), _P(ctypes.c_int)], ctypes.c_int),
     "ktune_cache_lookup_conv": ([ctypes.c_char_p, _P(ConvInputC), _P(ctypes.c_int)], ctypes.c_int),
     "ktune_cache_store": ([ctypes.c_char_p, ctypes.c_char_p], ctypes.c_int),
+    "ktune_select_conv": ([_P(HwC), ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, _P(ConvInputC),
+                           ctypes.c_int32, _P(ConvTuningC), _P(ctypes.c_int32)], ctypes.c_int),
+    "ktune_infer_gemm_shard": ([_P(HwC), ctypes.c_char_p, ctypes.c_char_p, _P(GemmInputC), ctypes.c_int32,
+                                ctypes.c_int32, _P(MeasureOptionsC), ctypes.c_int32, ctypes.c_int32, _vp,
+                                ctypes.c_int64, _P(ctypes.c_int64)], ctypes.c_int),
+    "ktune_infer_conv_shard": ([_P(HwC), ctypes.c_char_p, ctypes.c_char_p, _P(ConvInputC), ctypes.c_int32,
+                                ctypes.c_int32, _P(MeasureOptionsC), ctypes.c_int32, ctypes.c_int32, _vp,
+                                ctypes.c_int64, _P(ctypes.c_int64)], ctypes.c_int),
+    "ktune_infer_gemm_replay": ([_P(HwC), ctypes.c_char_p, ctypes.c_char_p, _P(GemmInputC), ctypes.c_int32,
+                                 ctypes.c_char_p, _vp, ctypes.c_int64], ctypes.c_int),
+    "ktune_infer_conv_replay": ([_P(HwC), ctypes.c_char_p, ctypes.c_char_p, _P(ConvInputC), ctypes.c_int32,
+                                 ctypes.c_char_p, _vp, ctypes.c_int64], ctypes.c_int),
     "ktune_select_gemm": ([_P(HwC), ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, _P(GemmInputC),
                            ctypes.c_int32, _P(GemmTuningC), _P(ctypes.c_int32)], ctypes.c_int),
     "ktune_cli_main": ([ctypes.c_int, _P(ctypes.c_char_p)], ctypes.c_int),

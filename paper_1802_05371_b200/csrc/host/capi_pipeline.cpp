@@ -109,6 +109,7 @@ std::unique_ptr<PerfPredictor> make_predictor(const char* model_json, const Hard
 // Runtime-selection memo: cache key -> chosen tuning (per process).
 std::mutex g_select_mu;
 std::map<std::string, GemmTuning> g_select_memo;
+std::map<std::string, ConvTuning> g_select_memo_conv;
 
 template <typename In, typename Tu, typename Draw, typename OutIn, typename OutTu>
 void shard_out(const std::vector<Draw>& draws, const std::vector<ShardRecord>& recs, const GenerateReport& rep,
@@ -130,6 +131,49 @@ void shard_out(const std::vector<Draw>& draws, const std::vector<ShardRecord>& r
     if (duplicates) *duplicates = rep.duplicates_rejected;
     if (unlaunchable) *unlaunchable = rep.unlaunchable_rejected;
 }
+
+// Sharded top-k re-measure (reference loop
+// pipeline.cpp:674-680): infer_* calls backend.measure once per ranked
+// candidate, in rank order.  ShardBackend measures the calls i with
+// i % world == rank and records them (others -> -1, never measured);
+// ReplayBackend feeds the gathered values back in the same order, so the
+// sharded result equals the sequential one.
+class ShardBackend final : public MeasurementBackend {
+  public:
+    ShardBackend(MeasurementBackend& real, int rank, int world) : real_(real), rank_(rank), world_(world) {
+        if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("shard: rank must lie in [0, world)");
+    }
+    std::string name() const override { return real_.name(); }
+    double measure(const GemmInput& in, const GemmTuning& t) override { return record(mine() ? real_.measure(in, t) : -1.0); }
+    double measure(const ConvInput& in, const ConvTuning& t) override { return record(mine() ? real_.measure(in, t) : -1.0); }
+    std::vector<double> values;
+
+  private:
+    bool mine() const { return int(values.size() % std::size_t(world_)) == rank_; }
+    double record(double v) {
+        values.push_back(v);
+        return v;
+    }
+    MeasurementBackend& real_;
+    int rank_, world_;
+};
+
+class ReplayBackend final : public MeasurementBackend {
+  public:
+    ReplayBackend(std::string name, const double* v, std::int64_t n) : name_(std::move(name)), v_(v), n_(n) {}
+    std::string name() const override { return name_; }
+    double measure(const GemmInput&, const GemmTuning&) override { return take(); }
+    double measure(const ConvInput&, const ConvTuning&) override { return take(); }
+
+  private:
+    double take() {
+        if (i_ >= n_) throw std::invalid_argument("infer replay: fewer measurements than candidates");
+        return v_[i_++];
+    }
+    std::string name_;
+    const double* v_;
+    std::int64_t n_, i_{0};
+};
 
 }  // namespace
 
@@ -451,6 +495,64 @@ int ktune_infer_conv(const ktune_hw* hw, const char* bounds_json, const char* mo
     });
 }
 
+int ktune_infer_gemm_shard(const ktune_hw* hw, const char* bounds_json, const char* model_json,
+                           const ktune_gemm_input* in, int32_t top_k, int32_t backend, const ktune_measure_options* opts,
+                           int32_t rank, int32_t world, double* gflops_out, int64_t cap, int64_t* count) {
+    return guard([&] {
+        need(gflops_out, "gflops_out");
+        need(count, "count");
+        const HardwareDescriptor h = conv_hw(hw);
+        auto be = make_backend(backend, h, opts);
+        ShardBackend sb(*be, rank, world);
+        auto pred = make_predictor(model_json, h);
+        (void)infer_gemm(*pred, conv_in(in), h, gemm_bounds(bounds_json), top_k, sb);
+        if (int64_t(sb.values.size()) > cap) throw std::invalid_argument("infer shard: cap smaller than top_k");
+        std::copy(sb.values.begin(), sb.values.end(), gflops_out);
+        *count = int64_t(sb.values.size());
+    });
+}
+
+int ktune_infer_conv_shard(const ktune_hw* hw, const char* bounds_json, const char* model_json,
+                           const ktune_conv_input* in, int32_t top_k, int32_t backend, const ktune_measure_options* opts,
+                           int32_t rank, int32_t world, double* gflops_out, int64_t cap, int64_t* count) {
+    return guard([&] {
+        need(gflops_out, "gflops_out");
+        need(count, "count");
+        const HardwareDescriptor h = conv_hw(hw);
+        auto be = make_backend(backend, h, opts);
+        ShardBackend sb(*be, rank, world);
+        auto pred = make_predictor(model_json, h);
+        (void)infer_conv(*pred, conv_in(in), h, conv_bounds(bounds_json), top_k, sb);
+        if (int64_t(sb.values.size()) > cap) throw std::invalid_argument("infer shard: cap smaller than top_k");
+        std::copy(sb.values.begin(), sb.values.end(), gflops_out);
+        *count = int64_t(sb.values.size());
+    });
+}
+
+int ktune_infer_gemm_replay(const ktune_hw* hw, const char* bounds_json, const char* model_json,
+                            const ktune_gemm_input* in, int32_t top_k, const char* backend_name, const double* gflops,
+                            int64_t n) {
+    return guard([&] {
+        need(gflops, "gflops");
+        const HardwareDescriptor h = conv_hw(hw);
+        ReplayBackend rb(backend_name ? backend_name : "b200", gflops, n);
+        auto pred = make_predictor(model_json, h);
+        last_text() = to_json_text(infer_gemm(*pred, conv_in(in), h, gemm_bounds(bounds_json), top_k, rb));
+    });
+}
+
+int ktune_infer_conv_replay(const ktune_hw* hw, const char* bounds_json, const char* model_json,
+                            const ktune_conv_input* in, int32_t top_k, const char* backend_name, const double* gflops,
+                            int64_t n) {
+    return guard([&] {
+        need(gflops, "gflops");
+        const HardwareDescriptor h = conv_hw(hw);
+        ReplayBackend rb(backend_name ? backend_name : "b200", gflops, n);
+        auto pred = make_predictor(model_json, h);
+        last_text() = to_json_text(infer_conv(*pred, conv_in(in), h, conv_bounds(bounds_json), top_k, rb));
+    });
+}
+
 int ktune_cache_key_gemm(const ktune_gemm_input* in) {
     return guard([&] { last_text() = cache_key(conv_in(in)); });
 }
@@ -526,6 +628,43 @@ int ktune_select_gemm(const ktune_hw* hw, const char* bounds_json, const char* m
         {
             std::lock_guard<std::mutex> lock(g_select_mu);
             g_select_memo[key] = r->chosen;
+        }
+        *chosen = out_t(r->chosen);
+        if (source) *source = src;
+    });
+}
+
+int ktune_select_conv(const ktune_hw* hw, const char* bounds_json, const char* model_json, const char* cache_dir,
+                      const ktune_conv_input* in, int32_t top_k, ktune_conv_tuning* chosen, int32_t* source) {
+    return guard([&] {
+        need(chosen, "chosen");
+        const ConvInput input = conv_in(in);
+        const HardwareDescriptor hwd = conv_hw(hw);
+        const std::string key = cache_key(input) + "|" + fnv1a64_hex(hwd.to_json_text()) + "|" +
+                                fnv1a64_hex(bounds_json ? bounds_json : "") + "|" +
+                                fnv1a64_hex(model_json ? model_json : "") + "|" + std::to_string(top_k);
+        {
+            std::lock_guard<std::mutex> lock(g_select_mu);
+            auto it = g_select_memo_conv.find(key);
+            if (it != g_select_memo_conv.end()) {
+                *chosen = out_t(it->second);
+                if (source) *source = 0;
+                return;
+            }
+        }
+        std::optional<ConvInferenceResult> r;
+        int32_t src = 1;
+        if (cache_dir && cache_dir[0]) r = ResultCache(cache_dir).lookup(input);
+        if (!r) {
+            B200Backend be(hwd);
+            auto pred = make_predictor(model_json, hwd);
+            r = infer_conv(*pred, input, hwd, conv_bounds(bounds_json), top_k, be);
+            if (cache_dir && cache_dir[0]) ResultCache(cache_dir).store(*r);
+            src = 2;
+        }
+        {
+            std::lock_guard<std::mutex> lock(g_select_mu);
+            g_select_memo_conv[key] = r->chosen;
         }
         *chosen = out_t(r->chosen);
         if (source) *source = src;

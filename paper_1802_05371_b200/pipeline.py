@@ -414,6 +414,56 @@ def infer(inp, hw: HardwareDescriptor, bounds_json: str | None = None, model_jso
     return _lib.text()
 
 
+def infer_sharded(inp, hw: HardwareDescriptor, bounds_json: str | None = None, model_json: str | None = None,
+                  top_k: int = 100, backend: str = "b200", mode: str = "fast", repetitions: int = 3, group=None,
+                  device=None) -> str:
+    """infer_* with the top-k re-measure sharded over the process group
+    (pipeline.cpp:674-680): each rank measures ranked
+    candidates i with i % world == rank, one all-reduce (max) of the
+    measurement vector, then every rank rebuilds the same ktune-result-1
+    JSON the sequential infer would write.  top_k >= the legal space is the
+    sharded `bench --exhaustive`."""
+    import torch
+    import torch.distributed as dist_
+
+    ws = dist_.get_world_size(group) if dist_.is_initialized() else 1
+    rank = dist_.get_rank(group) if dist_.is_initialized() else 0
+    conv = isinstance(inp, ConvInput)
+    opts = _lib.MeasureOptionsC(_lib.MODE_PARITY if mode == "parity" else _lib.MODE_FAST, repetitions, 1, 1, 0x5EED)
+    from . import enumerate_legal
+    cap = max(1, min(top_k, len(enumerate_legal(inp, hw, bounds_json))))
+    vals = np.full(cap, -1.0)
+    cnt = ctypes.c_int64()
+    ic = inp.cstruct() if conv else inp.c()
+    _lib.call("ktune_infer_conv_shard" if conv else "ktune_infer_gemm_shard", ctypes.byref(hw.c()),
+              _b(bounds_json or ""), _b(model_json or ""), ctypes.byref(ic), top_k, BACKENDS[backend],
+              ctypes.byref(opts), rank, ws, vals.ctypes.data_as(ctypes.c_void_p), cap, ctypes.byref(cnt))
+    vals = vals[: cnt.value]
+    if ws > 1:
+        dev = device if device is not None else ("cuda" if dist_.get_backend(group) == "nccl" else "cpu")
+        t = torch.from_numpy(vals.copy()).to(dev)
+        dist_.all_reduce(t, op=dist_.ReduceOp.MAX, group=group)
+        vals = t.cpu().numpy()
+    name = backend if backend != "b200" or mode == "fast" else "b200-parity"
+    vals = np.ascontiguousarray(vals, np.float64)
+    _lib.call("ktune_infer_conv_replay" if conv else "ktune_infer_gemm_replay", ctypes.byref(hw.c()),
+              _b(bounds_json or ""), _b(model_json or ""), ctypes.byref(ic), top_k, name.encode(),
+              vals.ctypes.data_as(ctypes.c_void_p), len(vals))
+    return _lib.text()
+
+
+def select_conv(inp: ConvInput, hw: HardwareDescriptor, bounds_json: str | None = None, model_json: str | None = None,
+                cache_dir: str | None = None, top_k: int = 100):
+    """Runtime pick for a convolution: memo -> result cache -> infer_conv
+    (b200).  Returns (ConvTuning, source) with source in {"memory", "file",
+    "inferred"}."""
+    t = _lib.ConvTuningC()
+    src = ctypes.c_int32()
+    _lib.call("ktune_select_conv", ctypes.byref(hw.c()), _b(bounds_json or ""), _b(model_json or ""),
+              _b(cache_dir or ""), ctypes.byref(inp.cstruct()), top_k, ctypes.byref(t), ctypes.byref(src))
+    return ConvTuning(*[getattr(t, n) for n in _lib.CONV_PARAMS]), ("memory", "file", "inferred")[src.value]
+
+
 def cache_key(inp) -> str:
     if isinstance(inp, ConvInput):
         _lib.call("ktune_cache_key_conv", ctypes.byref(inp.cstruct()))

@@ -193,3 +193,41 @@ def test_sharded_generation_two_ranks_matches_sequential(golden, tmp_path):
         assert sha(open(tmp_path / f"rank{r}.csv").read()) == g["csv_sha256"]
     stats = [json.load(open(tmp_path / f"rank{r}.json")) for r in range(2)]
     assert sum(s["local_samples"] for s in stats) == g["n"]
+
+
+def _infer_sharded_worker(rank, world, port, out):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        hw = K.HardwareDescriptor()
+        for inp in (K.GemmInput(2560, 16, 2560, "f32"), K.ConvInput(4, 9, 11, 24, 5, 3, 3)):
+            for k in (7, 1 << 30):  # top-k and the exhaustive bench
+                out.put((rank, type(inp).__name__, k, P.infer_sharded(inp, hw, None, None, k, backend="analytical")))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_infer_sharded_equals_sequential_on_gloo():
+    """the top-k re-measure (and the exhaustive bench)
+    sharded over 2 ranks rebuilds the sequential infer_* result JSON byte for
+    byte on every rank (analytical backend: deterministic measurements)."""
+    import socket
+
+    import torch.multiprocessing as mp
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_infer_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    got = [q.get(timeout=300) for _ in range(8)]
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    hw = K.HardwareDescriptor()
+    for rank, kind, k, text in got:
+        inp = K.GemmInput(2560, 16, 2560, "f32") if kind == "GemmInput" else K.ConvInput(4, 9, 11, 24, 5, 3, 3)
+        assert text == P.infer(inp, hw, None, None, k, backend="analytical"), (rank, kind, k)
