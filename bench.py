@@ -446,10 +446,23 @@ def tuning_loop(args, ws, rank, dev):
             out["ratio_vs_reference_host"] = out["samples_per_s"] / ref["samples_per_s"]
         t1 = time.perf_counter()
         fit = P.train_mlp(csv, epochs=60, seed=7)
-        out["mlp_fit"] = {"rows": n, "epochs": 60, "seconds": time.perf_counter() - t1,
-                          "best_val_mse": fit.best_val_mse}
+        t_exact = time.perf_counter() - t1
+        t1 = time.perf_counter()
+        fit_fast = P.train_mlp(csv, epochs=60, seed=7, fast=True)
+        t_fast = time.perf_counter() - t1
+        out["mlp_fit"] = {"rows": n, "epochs": 60, "seconds": t_exact, "best_val_mse": fit.best_val_mse,
+                          "where": "GPU K7 (reference operation order, one CTA)",
+                          "fast_seconds": t_fast, "fast_best_val_mse": fit_fast.best_val_mse,
+                          "fast_epoch_ms": t_fast / 60 * 1e3, "fast_where": "GPU K7f (batched fp64 GEMMs per layer)"}
         inp = K.GemmInput(2560, 32, 2560, "f32")
         space = K.enumerate_legal(inp, hw, bounds)
+        P.mlp_sweep(fit.model_json, inp, hw, bounds, fast=True)  # warm (cuBLAS handle, buffers)
+        ns, dev_s, tot_s = P.mlp_sweep(fit.model_json, inp, hw, bounds, fast=True)
+        ne, _, tot_e = P.mlp_sweep(fit.model_json, inp, hw, bounds, fast=False)
+        out["mlp_sweep"] = {"candidates": ns, "fast_device_predictions_per_s": ns / dev_s,
+                            "fast_call_predictions_per_s": ns / tot_s, "exact_call_predictions_per_s": ne / tot_e,
+                            "note": "K6f: one fp64 GEMM per layer over all candidates (device time of features + "
+                                    "layers); K6: bit-identical per-candidate fp64 (whole call, in the library)"}
         P.mlp_predict(fit.model_json, inp, space[:1000])
         t2 = time.perf_counter()
         P.mlp_predict(fit.model_json, inp, space)
@@ -910,6 +923,10 @@ def our_arm(args):
         line["tuning"]["cpu_cores"] = cb.get("cores")
         if "mlp_fit" in t:
             line["tuning"]["mlp_fit_s"] = round(t["mlp_fit"]["seconds"], 3)
+            line["tuning"]["mlp_fit_fast_s"] = round(t["mlp_fit"]["fast_seconds"], 3)
+        if "mlp_sweep" in t:
+            line["tuning"]["sweep_fast_dev_pred_per_s"] = round(t["mlp_sweep"]["fast_device_predictions_per_s"])
+            line["tuning"]["sweep_exact_pred_per_s"] = round(t["mlp_sweep"]["exact_call_predictions_per_s"])
         if rp:
             line["tuning"]["sweep_pred_per_s"] = round(rp["sweep_predictions_per_s"])
             line["tuning"]["warm_pick_us"] = round(rp["warm_pick_us"], 1)

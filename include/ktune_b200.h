@@ -299,11 +299,28 @@ KTUNE_API int ktune_mlp_train(const char* csv_text, int32_t kind, const int32_t*
                               uint64_t seed, double validation_fraction, double* best_val_mse, int32_t* best_epoch,
                               double* history);
 /* Glorot init (perf_model.cpp:57-79) as a model JSON. */
+/* K7f: the same training (loss, shuffles, minibatches, clip, best epoch) with
+ * every layer of a minibatch as one batched fp64 GEMM (GEMM summation order:
+ * rounding-level differences from ktune_mlp_train). */
+KTUNE_API int ktune_mlp_train_fast(const char* csv_text, int32_t kind, const int32_t* hidden, int32_t n_hidden,
+                                   int32_t log_inputs, int32_t epochs, double learning_rate, int32_t batch_size,
+                                   uint64_t seed, double validation_fraction, double* best_val_mse,
+                                   int32_t* best_epoch, double* history);
+/* The runtime candidate sweep over the whole legal space of `in` (enumerated
+ * in the library, no per-candidate marshalling): fast = 0 K6 (bit-identical),
+ * 1 K6f (batched GEMMs).  *device_seconds = GPU time of the sweep (K6f) or
+ * the whole call (K6); *total_seconds = the whole call. */
+KTUNE_API int ktune_mlp_sweep_gemm(const char* model_json, const ktune_hw* hw, const char* bounds_json,
+                                   const ktune_gemm_input* in, int32_t fast, int64_t* n_candidates,
+                                   double* device_seconds, double* total_seconds);
 KTUNE_API int ktune_mlp_init(int32_t input_dim, const int32_t* hidden, int32_t n_hidden, int32_t log_inputs,
                              uint64_t seed, const char* feature_version);
 /* GPU forward of raw feature rows (MlpModel::predict_batch, bit-exact). */
 KTUNE_API int ktune_mlp_predict_rows(const char* model_json, const double* rows, int64_t n, int32_t dim, double* out);
 /* GPU candidate sweep for one GEMM / CONV input (MlpPredictor::predict_*). */
+/* K6f predictions (batched GEMMs, rounding-level differences from K6). */
+KTUNE_API int ktune_mlp_predict_gemm_fast(const char* model_json, const ktune_gemm_input* in,
+                                          const ktune_gemm_tuning* tunings, int64_t n, double* out);
 KTUNE_API int ktune_mlp_predict_gemm(const char* model_json, const ktune_gemm_input* in,
                                      const ktune_gemm_tuning* tunings, int64_t n, double* out);
 KTUNE_API int ktune_mlp_predict_conv(const char* model_json, const ktune_conv_input* in,

@@ -181,10 +181,16 @@ _SIGNATURES = {
     "ktune_mlp_train": ([ctypes.c_char_p, ctypes.c_int32, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                          ctypes.c_double, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double, _P(ctypes.c_double),
                          _P(ctypes.c_int32), _vp], ctypes.c_int),
+    "ktune_mlp_train_fast": ([ctypes.c_char_p, ctypes.c_int32, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                         ctypes.c_double, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double, _P(ctypes.c_double),
+                         _P(ctypes.c_int32), _vp], ctypes.c_int),
+    "ktune_mlp_sweep_gemm": ([ctypes.c_char_p, _P(HwC), ctypes.c_char_p, _P(GemmInputC), ctypes.c_int32,
+                              _P(ctypes.c_int64), _P(ctypes.c_double), _P(ctypes.c_double)], ctypes.c_int),
     "ktune_mlp_init": ([ctypes.c_int32, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_char_p],
                        ctypes.c_int),
     "ktune_mlp_predict_rows": ([ctypes.c_char_p, _vp, _i64, ctypes.c_int32, _vp], ctypes.c_int),
     "ktune_mlp_predict_gemm": ([ctypes.c_char_p, _P(GemmInputC), _vp, _i64, _vp], ctypes.c_int),
+    "ktune_mlp_predict_gemm_fast": ([ctypes.c_char_p, _P(GemmInputC), _vp, _i64, _vp], ctypes.c_int),
     "ktune_mlp_predict_conv": ([ctypes.c_char_p, _P(ConvInputC), _vp, _i64, _vp], ctypes.c_int),
     "ktune_mlp_evaluate": ([ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int32, _P(ctypes.c_double)], ctypes.c_int),
     "ktune_infer_gemm": ([_P(HwC), ctypes.c_char_p, ctypes.c_char_p, _P(GemmInputC), ctypes.c_int32,

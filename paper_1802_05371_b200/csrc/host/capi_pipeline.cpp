@@ -2,6 +2,7 @@
 // (sampler, predraw/generation, datasets, MLP, runtime selection, cache);
 // declarations and reference citations in include/ktune_b200.h.
 
+#include <chrono>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -379,9 +380,50 @@ int ktune_dataset_canonical(const char* csv_text, int32_t kind) {
     });
 }
 
+namespace {
+int mlp_train_impl(const char* csv_text, int32_t kind, const int32_t* hidden, int32_t n_hidden, int32_t log_inputs,
+                   int32_t epochs, double learning_rate, int32_t batch_size, uint64_t seed, double validation_fraction,
+                   double* best_val_mse, int32_t* best_epoch, double* history, bool fast);
+}
+
 int ktune_mlp_train(const char* csv_text, int32_t kind, const int32_t* hidden, int32_t n_hidden, int32_t log_inputs,
                     int32_t epochs, double learning_rate, int32_t batch_size, uint64_t seed, double validation_fraction,
                     double* best_val_mse, int32_t* best_epoch, double* history) {
+    return mlp_train_impl(csv_text, kind, hidden, n_hidden, log_inputs, epochs, learning_rate, batch_size, seed,
+                          validation_fraction, best_val_mse, best_epoch, history, false);
+}
+
+int ktune_mlp_train_fast(const char* csv_text, int32_t kind, const int32_t* hidden, int32_t n_hidden,
+                         int32_t log_inputs, int32_t epochs, double learning_rate, int32_t batch_size, uint64_t seed,
+                         double validation_fraction, double* best_val_mse, int32_t* best_epoch, double* history) {
+    return mlp_train_impl(csv_text, kind, hidden, n_hidden, log_inputs, epochs, learning_rate, batch_size, seed,
+                          validation_fraction, best_val_mse, best_epoch, history, true);
+}
+
+int ktune_mlp_sweep_gemm(const char* model_json, const ktune_hw* hw, const char* bounds_json,
+                         const ktune_gemm_input* in, int32_t fast, int64_t* n_candidates, double* device_seconds,
+                         double* total_seconds) {
+    return guard([&] {
+        need(model_json, "model_json");
+        const HardwareDescriptor h = conv_hw(hw);
+        const std::vector<GemmTuning> legal = enumerate_legal(conv_in(in), h, gemm_bounds(bounds_json));
+        MlpPredictor p(MlpModel::from_json_text(model_json), fast != 0);
+        std::vector<double> out;
+        const auto t0 = std::chrono::steady_clock::now();
+        p.predict_gemm(conv_in(in), legal, out);
+        const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (n_candidates) *n_candidates = int64_t(legal.size());
+        if (device_seconds) *device_seconds = fast ? p.last_device_seconds() : secs;
+        if (total_seconds) *total_seconds = secs;
+    });
+}
+
+}  // extern "C"
+
+namespace {
+int mlp_train_impl(const char* csv_text, int32_t kind, const int32_t* hidden, int32_t n_hidden, int32_t log_inputs,
+                   int32_t epochs, double learning_rate, int32_t batch_size, uint64_t seed, double validation_fraction,
+                   double* best_val_mse, int32_t* best_epoch, double* history, bool fast) {
     return guard([&] {
         need(csv_text, "csv_text");
         const TrainingSet set = kind == 0 ? to_training_set(gemm_dataset_from_csv_text(csv_text))
@@ -396,6 +438,7 @@ int ktune_mlp_train(const char* csv_text, int32_t kind, const int32_t* hidden, i
         cfg.batch_size = batch_size;
         cfg.rng_seed = seed;
         cfg.validation_fraction = validation_fraction;
+        cfg.fast = fast;
         TrainResult r = mlp_train(set, arch, cfg);
         if (best_val_mse) *best_val_mse = r.best_val_mse;
         if (best_epoch) *best_epoch = r.best_epoch;
@@ -410,6 +453,9 @@ int ktune_mlp_train(const char* csv_text, int32_t kind, const int32_t* hidden, i
         last_text() = m.to_json_text();
     });
 }
+}  // namespace
+
+extern "C" {
 
 int ktune_mlp_init(int32_t input_dim, const int32_t* hidden, int32_t n_hidden, int32_t log_inputs, uint64_t seed,
                    const char* feature_version) {
@@ -433,6 +479,19 @@ int ktune_mlp_predict_rows(const char* model_json, const double* rows, int64_t n
         for (int64_t i = 0; i < n; ++i) r[std::size_t(i)].assign(rows + i * dim, rows + (i + 1) * dim);
         std::vector<double> o;
         m.predict_batch(r, o);
+        std::memcpy(out, o.data(), o.size() * sizeof(double));
+    });
+}
+
+int ktune_mlp_predict_gemm_fast(const char* model_json, const ktune_gemm_input* in,
+                                const ktune_gemm_tuning* tunings, int64_t n, double* out) {
+    return guard([&] {
+        need(model_json, "model_json");
+        MlpPredictor p(MlpModel::from_json_text(model_json), true);
+        std::vector<GemmTuning> ts;
+        for (int64_t i = 0; i < n; ++i) ts.push_back(conv_t(tunings + i));
+        std::vector<double> o;
+        p.predict_gemm(conv_in(in), ts, o);
         std::memcpy(out, o.data(), o.size() * sizeof(double));
     });
 }

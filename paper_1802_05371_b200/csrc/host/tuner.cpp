@@ -594,7 +594,9 @@ double AnalyticalBackend::measure(const ConvInput& in, const ConvTuning& t) { re
 // predictors
 // ---------------------------------------------------------------------------
 
-MlpPredictor::MlpPredictor(MlpModel model) : model_(std::move(model)) { model_.weights.validate(); }
+MlpPredictor::MlpPredictor(MlpModel model, bool fast) : model_(std::move(model)), fast_(fast) {
+    model_.weights.validate();
+}
 std::string MlpPredictor::name() const { return "mlp"; }
 
 void MlpPredictor::predict_gemm(const GemmInput& input, const std::vector<GemmTuning>& tunings,
@@ -613,7 +615,9 @@ void MlpPredictor::predict_gemm(const GemmInput& input, const std::vector<GemmTu
                                    double(dtype_size_bytes(input.dtype)), input.trans_a ? 2.0 : 1.0,
                                    input.trans_b ? 2.0 : 1.0};
     out.resize(tunings.size());
-    mlp_predict_tuples(model_.weights, head, flat.data(), std::int64_t(tunings.size()), 8, out.data());
+    if (fast_) mlp_predict_tuples_fast(model_.weights, head, flat.data(), std::int64_t(tunings.size()), 8, out.data(),
+                                       &last_device_s_);
+    else mlp_predict_tuples(model_.weights, head, flat.data(), std::int64_t(tunings.size()), 8, out.data());
 }
 
 void MlpPredictor::predict_conv(const ConvInput& input, const std::vector<ConvTuning>& tunings,
@@ -631,7 +635,9 @@ void MlpPredictor::predict_conv(const ConvInput& input, const std::vector<ConvTu
     const std::vector<double> head{double(input.n_batch), double(input.p), double(input.q), double(input.k_filters),
                                    double(input.c),       double(input.r), double(input.s)};
     out.resize(tunings.size());
-    mlp_predict_tuples(model_.weights, head, flat.data(), std::int64_t(tunings.size()), 12, out.data());
+    if (fast_) mlp_predict_tuples_fast(model_.weights, head, flat.data(), std::int64_t(tunings.size()), 12, out.data(),
+                                       &last_device_s_);
+    else mlp_predict_tuples(model_.weights, head, flat.data(), std::int64_t(tunings.size()), 12, out.data());
 }
 
 AnalyticalPredictor::AnalyticalPredictor(HardwareDescriptor hw) : hw_(std::move(hw)) { hw_.validate(); }

@@ -359,6 +359,7 @@ void mlp_predict_tuples(const MlpWeights& w, const std::vector<double>& const_fe
 
 TrainResult mlp_train(const TrainingSet& train, const TrainingSet& val, const MlpArchitecture& arch,
                       const TrainConfig& cfg) {
+    if (cfg.fast) return mlp_train_fast(train, val, arch, cfg);
     arch.validate();
     cfg.validate();
     train.validate();

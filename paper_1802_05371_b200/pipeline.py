@@ -337,12 +337,14 @@ class TrainOutcome:
 
 
 def train_mlp(csv_text: str, kind: str = "gemm", hidden=(32, 64, 32), log_inputs=True, epochs=200, lr=1e-3,
-              batch_size=256, seed=0, validation_fraction=0.1) -> TrainOutcome:
+              batch_size=256, seed=0, validation_fraction=0.1, fast=False) -> TrainOutcome:
+    """K7 (reference operation order, bit-identical models) or, with fast,
+    K7f (each minibatch layer one batched fp64 GEMM)."""
     hid = (ctypes.c_int32 * len(hidden))(*hidden)
     hist = np.zeros((epochs, 2))
     bv, be = ctypes.c_double(), ctypes.c_int32()
-    _lib.call("ktune_mlp_train", csv_text.encode(), 0 if kind == "gemm" else 1, ctypes.cast(hid, ctypes.c_void_p),
-              len(hidden), int(log_inputs), epochs, lr, batch_size, seed, validation_fraction, ctypes.byref(bv),
+    _lib.call("ktune_mlp_train_fast" if fast else "ktune_mlp_train", csv_text.encode(), 0 if kind == "gemm" else 1,
+              ctypes.cast(hid, ctypes.c_void_p), len(hidden), int(log_inputs), epochs, lr, batch_size, seed, validation_fraction, ctypes.byref(bv),
               ctypes.byref(be), hist.ctypes.data_as(ctypes.c_void_p))
     return TrainOutcome(_lib.text(), bv.value, be.value, hist)
 
@@ -362,12 +364,14 @@ def mlp_predict_rows(model_json: str, rows) -> np.ndarray:
     return out
 
 
-def mlp_predict(model_json: str, inp, tunings) -> np.ndarray:
-    """GPU candidate sweep (MlpPredictor::predict_*, bit-exact)."""
+def mlp_predict(model_json: str, inp, tunings, fast: bool = False) -> np.ndarray:
+    """GPU candidate sweep (MlpPredictor::predict_*): K6 bit-exact, or K6f
+    (batched GEMMs) with fast (GEMM inputs only)."""
     conv = isinstance(inp, ConvInput)
     arr = ((_lib.ConvTuningC if conv else _lib.GemmTuningC) * len(tunings))(*[t.c() for t in tunings])
     out = np.zeros(len(tunings))
-    _lib.call("ktune_mlp_predict_conv" if conv else "ktune_mlp_predict_gemm", model_json.encode(),
+    fn = "ktune_mlp_predict_conv" if conv else ("ktune_mlp_predict_gemm_fast" if fast else "ktune_mlp_predict_gemm")
+    _lib.call(fn, model_json.encode(),
               ctypes.byref(inp.cstruct() if conv else inp.c()), ctypes.cast(arr, ctypes.c_void_p), len(tunings),
               out.ctypes.data_as(ctypes.c_void_p))
     return out
@@ -412,6 +416,16 @@ def infer(inp, hw: HardwareDescriptor, bounds_json: str | None = None, model_jso
         _lib.call("ktune_infer_gemm", ctypes.byref(hw.c()), _b(bounds_json or ""), _b(model_json or ""),
                   ctypes.byref(inp.c()), top_k, BACKENDS[backend], ctypes.byref(opts))
     return _lib.text()
+
+
+def mlp_sweep(model_json: str, inp: GemmInput, hw: HardwareDescriptor, bounds_json: str | None = None,
+              fast: bool = False):
+    """The runtime candidate sweep over the whole legal space, entirely in the
+    library: returns (candidates, device_seconds, total_seconds)."""
+    n, dsec, tsec = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
+    _lib.call("ktune_mlp_sweep_gemm", model_json.encode(), ctypes.byref(hw.c()), _b(bounds_json or ""),
+              ctypes.byref(inp.c()), 1 if fast else 0, ctypes.byref(n), ctypes.byref(dsec), ctypes.byref(tsec))
+    return n.value, dsec.value, tsec.value
 
 
 def infer_sharded(inp, hw: HardwareDescriptor, bounds_json: str | None = None, model_json: str | None = None,
