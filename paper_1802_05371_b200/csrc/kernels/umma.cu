@@ -557,6 +557,14 @@ struct TcPlan {
     dim3 grid;
     std::size_t smem{0};
     std::size_t ws_bytes{0};
+    // operand staging (any-shape contract of execute_gemm, backends.cpp:228-329):
+    // an operand whose leading dimension is not a 16-byte multiple (TMA) is
+    // copied into a padded workspace copy; a tf32 operand in MN-major layout
+    // is transposed into a K-major copy (tcgen05 kind::tf32 reads K-major)
+    bool stage_a{false}, stage_b{false};
+    bool tr_a{false}, tr_b{false};           // transpose while staging
+    std::int64_t a_ld{0}, b_ld{0};           // leading dimension (elements) the kernel reads
+    std::size_t a_stage_off{0}, b_stage_off{0}, stage_bytes{0};
     int kind{0};
     int ksteps{4};
     bool pair{false};  // m_l = 256: cluster of two CTAs, tcgen05.mma.cta_group::2
@@ -599,9 +607,12 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     p.umma_k_bytes = 32;
     p.a_kmajor = in.trans_a ? 0 : 1;
     p.b_kmajor = in.trans_b ? 1 : 0;
-    if (in.dtype == Dtype::tf32 && !(p.a_kmajor && p.b_kmajor))
-        throw unsupported_error("tensor-core family: tf32 needs K-major operands (trans_a = 0, trans_b = 1); "
-                                "MN-major tf32 tiles are not supported by this build");
+    if (in.dtype == Dtype::tf32) {
+        // kind::tf32 tiles are K-major here: stage MN-major operands transposed
+        pl.tr_a = !p.a_kmajor;
+        pl.tr_b = !p.b_kmajor;
+        p.a_kmajor = p.b_kmajor = 1;
+    }
     // swizzle spans and TMA boxes
     auto span_for = [](int bytes) { return bytes >= 128 ? 128 : (bytes >= 64 ? 64 : 32); };
     if (p.a_kmajor) {
@@ -645,9 +656,16 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     p.a_tile_bytes = unsigned(ceil_div(std::int64_t(p.a_boxes) * p.a_box_stride, 1024) * 1024);
     p.b_tile_bytes = unsigned(ceil_div(std::int64_t(p.b_boxes) * p.b_box_stride, 1024) * 1024);
     // TMA: global strides must be multiples of 16 bytes
-    const std::int64_t a_ld = in.trans_a ? in.m : in.k, b_ld = in.trans_b ? in.k : in.n;
-    if ((a_ld * es) % 16 != 0 || (b_ld * es) % 16 != 0)
-        throw unsupported_error("tensor-core family: leading dimensions must be multiples of 16 bytes for TMA");
+    // leading dimensions the kernel reads (after staging): TMA needs 16-byte
+    // multiples; other operands are staged into padded (or transposed) copies
+    const int align = 16 / es;
+    auto padded = [&](std::int64_t x) { return (x + align - 1) / align * align; };
+    const std::int64_t a_ld0 = p.a_kmajor ? in.k : in.m, b_ld0 = p.b_kmajor ? in.k : in.n;
+    const std::int64_t a_src_ld = in.trans_a ? in.m : in.k, b_src_ld = in.trans_b ? in.k : in.n;
+    pl.stage_a = pl.tr_a || (a_src_ld * es) % 16 != 0;
+    pl.stage_b = pl.tr_b || (b_src_ld * es) % 16 != 0;
+    pl.a_ld = pl.stage_a ? padded(a_ld0) : a_ld0;
+    pl.b_ld = pl.stage_b ? padded(b_ld0) : b_ld0;
     p.kb_total = int(ceil_div(in.k, p.bk));
     const std::size_t stage_bytes = std::size_t(p.a_tile_bytes) + p.b_tile_bytes;
     const std::size_t extra = 1024 + 8 * 32 + 64;  // alignment slack + barriers (2*stages + 4) + tmem slot
@@ -720,11 +738,65 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
         pl.ws_bytes = dev::kSplitCounterBytes +
                       std::size_t(p.smax + p.gmax) * std::size_t(in.m) * std::size_t(in.n) * sizeof(float);
     }
+    if (pl.stage_a || pl.stage_b) {
+        // staged operand copies after the split-K region (256-byte aligned)
+        if (pl.ws_bytes == 0) pl.ws_bytes = dev::kSplitCounterBytes;
+        auto take = [&](std::size_t bytes) {
+            const std::size_t off = (pl.ws_bytes + 255) / 256 * 256;
+            pl.ws_bytes = off + bytes;
+            return off;
+        };
+        if (pl.stage_a)
+            pl.a_stage_off = take(std::size_t(pl.a_ld) * std::size_t(p.a_kmajor ? in.m : in.k) * std::size_t(es));
+        if (pl.stage_b)
+            pl.b_stage_off = take(std::size_t(pl.b_ld) * std::size_t(p.b_kmajor ? in.n : in.k) * std::size_t(es));
+    }
     return pl;
 }
 
 
 }  // namespace
+
+// Staging copy: dst (rows x cols, leading dimension ld_dst) from src (row
+// major rows x cols with ld_src, or transposed: src is cols x rows); 32x32
+// tiles through shared memory so both sides stay coalesced.
+template <typename E>
+__global__ void stage_kernel(const E* __restrict__ src, std::int64_t ld_src, E* __restrict__ dst, std::int64_t ld_dst,
+                             std::int64_t rows, std::int64_t cols, int transpose) {
+    __shared__ E tile[32][33];
+    const std::int64_t r0 = std::int64_t(blockIdx.y) * 32, c0 = std::int64_t(blockIdx.x) * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+    for (int i = ty; i < 32; i += 8) {
+        // read: transposed source element (c, r) lives at src[c * ld_src + r]
+        const std::int64_t r = transpose ? c0 + i : r0 + i, c = transpose ? r0 + tx : c0 + tx;
+        const std::int64_t sr = transpose ? r : r, sc = c;
+        const bool ok = transpose ? (r < cols && c < rows) : (r < rows && c < cols);
+        tile[i][tx] = ok ? src[sr * ld_src + sc] : E(0);
+    }
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8) {
+        const std::int64_t r = r0 + i, c = c0 + tx;
+        if (r < rows && c < cols) dst[r * ld_dst + c] = transpose ? tile[tx][i] : tile[i][tx];
+    }
+}
+
+void stage(const void* src, std::int64_t ld_src, void* dst, std::int64_t ld_dst, std::int64_t rows, std::int64_t cols,
+           bool transpose, int es, cudaStream_t s) {
+    if (!transpose) {
+        dev::check(cudaMemcpy2DAsync(dst, std::size_t(ld_dst) * es, src, std::size_t(ld_src) * es,
+                                     std::size_t(cols) * es, std::size_t(rows), cudaMemcpyDeviceToDevice, s),
+                   "stage copy");
+        return;
+    }
+    const dim3 grid(unsigned((cols + 31) / 32), unsigned((rows + 31) / 32)), block(32, 8);
+    if (es == 4)
+        stage_kernel<unsigned><<<grid, block, 0, s>>>(static_cast<const unsigned*>(src), ld_src,
+                                                      static_cast<unsigned*>(dst), ld_dst, rows, cols, 1);
+    else
+        stage_kernel<unsigned short><<<grid, block, 0, s>>>(static_cast<const unsigned short*>(src), ld_src,
+                                                            static_cast<unsigned short*>(dst), ld_dst, rows, cols, 1);
+    dev::check(cudaGetLastError(), "stage transpose launch");
+}
 
 std::size_t gemm_workspace_bytes(const GemmInput& in, const GemmTuning& t) { return tc_plan(in, t).ws_bytes; }
 
@@ -742,10 +814,25 @@ void gemm(const GemmInput& in, const GemmTuning& t, const void* a, const void* b
         throw unsupported_error("tensor-core family: operand pointers must be 16-byte aligned for TMA");
     p.C = static_cast<float*>(c);
     if (const char* d = std::getenv("KTUNE_TC_DEBUG")) p.dbg = reinterpret_cast<long long*>(std::strtoull(d, nullptr, 0));
+    if (pl.ws_bytes > 0 && (ws == nullptr || ws_bytes < pl.ws_bytes))
+        throw workspace_error("workspace of " + std::to_string(ws_bytes) + " bytes is smaller than the " +
+                              std::to_string(pl.ws_bytes) + " bytes this tuning needs");
+    const int es0 = p.esize;
+    if (pl.stage_a) {
+        // A is M x K (ld K) or, transposed, K x M (ld M); the kernel reads the layout p.a_kmajor says
+        void* dst = static_cast<unsigned char*>(ws) + pl.a_stage_off;
+        if (p.a_kmajor) stage(a, in.trans_a ? in.m : in.k, dst, pl.a_ld, in.m, in.k, pl.tr_a, es0, stream);
+        else stage(a, in.m, dst, pl.a_ld, in.k, in.m, false, es0, stream);
+        a = dst;
+    }
+    if (pl.stage_b) {
+        // B is K x N (ld N) or, transposed, N x K (ld K)
+        void* dst = static_cast<unsigned char*>(ws) + pl.b_stage_off;
+        if (p.b_kmajor) stage(b, in.trans_b ? in.k : in.n, dst, pl.b_ld, in.n, in.k, pl.tr_b, es0, stream);
+        else stage(b, in.n, dst, pl.b_ld, in.k, in.n, false, es0, stream);
+        b = dst;
+    }
     if (p.smax > 1) {
-        if (ws == nullptr || ws_bytes < pl.ws_bytes)
-            throw workspace_error("workspace of " + std::to_string(ws_bytes) + " bytes is smaller than the " +
-                                  std::to_string(pl.ws_bytes) + " bytes this tuning needs");
         // arrival counters in the zeroed counter region (kernels.hpp), then
         // the segment and fold-group partials
         p.counters = static_cast<unsigned*>(ws);
@@ -754,10 +841,10 @@ void gemm(const GemmInput& in, const GemmTuning& t, const void* a, const void* b
     }
     const int es = p.esize;
     // A: K-major -> [M][K] rows, boxes {a_sw/es along K, bm}; MN-major -> [K][M], boxes {a_sw/es along M, bk}
-    CUtensorMap ma = p.a_kmajor ? make_map(a, in.dtype, in.k, in.m, p.a_sw / es, p.a_rows, p.a_sw)
-                                : make_map(a, in.dtype, in.m, in.k, p.a_sw / es, p.bk, p.a_sw);
-    CUtensorMap mb = p.b_kmajor ? make_map(b, in.dtype, in.k, in.n, p.b_sw / es, p.b_rows, p.b_sw)
-                                : make_map(b, in.dtype, in.n, in.k, p.b_sw / es, p.bk, p.b_sw);
+    CUtensorMap ma = p.a_kmajor ? make_map(a, in.dtype, in.k, in.m, p.a_sw / es, p.a_rows, p.a_sw, pl.a_ld)
+                                : make_map(a, in.dtype, in.m, in.k, p.a_sw / es, p.bk, p.a_sw, pl.a_ld);
+    CUtensorMap mb = p.b_kmajor ? make_map(b, in.dtype, in.k, in.n, p.b_sw / es, p.b_rows, p.b_sw, pl.b_ld)
+                                : make_map(b, in.dtype, in.n, in.k, p.b_sw / es, p.bk, p.b_sw, pl.b_ld);
     using ktune_dev::tc::umma_gemm_kernel;
 #define KTUNE_TC_ROW(K, P)                                                                           \
     {reinterpret_cast<const void*>(&umma_gemm_kernel<K, 1, P>), reinterpret_cast<const void*>(&umma_gemm_kernel<K, 2, P>), \

@@ -283,11 +283,11 @@ inline CUtensorMapSwizzle tma_swizzle(int sw) {
 
 // 2-D map over a row-major [outer][inner] matrix; box = {box_inner, box_outer}.
 inline CUtensorMap make_map(const void* base, Dtype dt, std::int64_t inner, std::int64_t outer, int box_inner, int box_outer,
-                     int sw) {
+                     int sw, std::int64_t ld = 0) {
     CUtensorMap m;
     const int es = dtype_size_bytes(dt);
     cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
-    cuuint64_t strides[1] = {cuuint64_t(inner) * cuuint64_t(es)};
+    cuuint64_t strides[1] = {cuuint64_t(ld > 0 ? ld : inner) * cuuint64_t(es)};
     cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_outer)};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode_fn()(&m, tma_dtype(dt), 2, const_cast<void*>(base), dims, strides, box, estr,

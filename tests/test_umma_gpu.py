@@ -52,11 +52,7 @@ def run(inp, t, seed=0):
 def test_layouts_and_dtypes(cuda, dtype, ta, tb):
     u = 64 if dtype != "tf32" else 32
     inp = K.GemmInput(256, 384, 512, dtype, ta, tb)
-    if dtype == "tf32" and (ta or not tb):
-        # tf32 tiles must be K-major on both operands in this build
-        with pytest.raises(K.Unsupported, match="tf32 needs K-major"):
-            run(inp, K.GemmTuning(8, 8, 128, 128, u, 1, 1, 1))
-        return
+    # tf32 MN-major operands are staged transposed into K-major workspace copies
     got, ref = run(inp, K.GemmTuning(8, 8, 128, 128, u, 1, 1, 1))
     assert O.max_rel_error(got, ref) < tol(inp.k)
 
@@ -65,7 +61,7 @@ def test_layouts_and_dtypes(cuda, dtype, ta, tb):
 @pytest.mark.parametrize("u", [32, 64, 128])
 def test_tile_shapes_bf16(cuda, n_l, u):
     # ragged against every tile extent; leading dimensions stay multiples of
-    # 16 bytes as TMA requires (unaligned ones raise Unsupported, below)
+    # 16 bytes (unaligned ones are staged: test_unaligned_leading_dimensions_staged)
     inp = K.GemmInput(300, 336, 712, "bf16", False, False)
     got, ref = run(inp, K.GemmTuning(8, 8, 128, n_l, u, 1, 1, 1), seed=n_l + u)
     assert O.max_rel_error(got, ref) < tol(inp.k)
@@ -109,10 +105,30 @@ def test_large_square_sampled(cuda):
 
 
 def test_unsupported_tuples_fail_loudly(cuda):
-    with pytest.raises(K.Unsupported, match="16 bytes for TMA"):
-        K.gemm_workspace_size(K.GemmInput(300, 333, 700, "bf16"), K.GemmTuning(8, 8, 128, 64, 64, 1, 1, 1))
     a = torch.zeros(64 * 64, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(K.Unsupported, match="m_l"):
         K.execute_gemm(K.GemmInput(64, 64, 64, "bf16"), K.GemmTuning(8, 8, 32, 64, 64, 1, 1, 1), a, a)
     with pytest.raises(K.Unsupported, match="k_l"):
         K.execute_gemm(K.GemmInput(64, 64, 64, "bf16"), K.GemmTuning(8, 8, 128, 64, 64, 1, 2, 1), a, a)
+
+
+@pytest.mark.parametrize("m,n,k,ta,tb", [
+    (300, 333, 700, False, False),   # N and K not multiples of 8 (16 bytes of bf16): both staged padded
+    (257, 129, 1001, True, False),
+    (100, 37, 515, False, True),
+    (33, 17, 9999, True, True),
+])
+def test_unaligned_leading_dimensions_staged(cuda, m, n, k, ta, tb):
+    """execute_gemm's any-shape contract (backends.cpp:228-329): operands
+    whose leading dimension TMA cannot stride are copied into padded
+    workspace copies first."""
+    inp = K.GemmInput(m, n, k, "bf16", ta, tb)
+    got, ref = run(inp, K.GemmTuning(8, 8, 128, 64, 64, 1, 1, 2))
+    assert O.max_rel_error(got, ref) < tol(k)
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (True, True)])
+def test_tf32_mn_major_square(cuda, ta, tb):
+    inp = K.GemmInput(512, 384, 640, "tf32", ta, tb)
+    got, ref = run(inp, K.GemmTuning(8, 8, 256, 128, 32, 1, 1, 1))
+    assert O.max_rel_error(got, ref) < tol(640)
