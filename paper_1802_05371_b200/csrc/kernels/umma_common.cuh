@@ -299,7 +299,10 @@ inline CUtensorMap make_map(const void* base, Dtype dt, std::int64_t inner, std:
 
 // N-D map over a dense tensor (dims innermost first, element strides are the
 // running products); zero fill outside the tensor.
-inline CUtensorMap make_map_nd(const void* base, Dtype dt, int rank, const std::int64_t* dims, const int* box, int sw) {
+// ld0 > 0: the innermost dimension is stored with that pitch (elements),
+// e.g. a padded staging copy; outer dimensions stay dense over it.
+inline CUtensorMap make_map_nd(const void* base, Dtype dt, int rank, const std::int64_t* dims, const int* box, int sw,
+                               std::int64_t ld0 = 0) {
     CUtensorMap m;
     const int es = dtype_size_bytes(dt);
     cuuint64_t gd[5], gs[4];
@@ -310,7 +313,7 @@ inline CUtensorMap make_map_nd(const void* base, Dtype dt, int rank, const std::
         bx[i] = cuuint32_t(box[i]);
         estr[i] = 1;
         if (i > 0) gs[i - 1] = cuuint64_t(stride);
-        stride *= dims[i];
+        stride *= (i == 0 && ld0 > 0) ? ld0 : dims[i];
     }
     CUresult r = encode_fn()(&m, tma_dtype(dt), cuuint32_t(rank), const_cast<void*>(base), gd, gs, bx, estr,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, tma_swizzle(sw), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

@@ -385,6 +385,10 @@ struct ConvPlan {
     dim3 grid;
     std::size_t smem{0};
     std::size_t ws_bytes{0}, flag_bytes{0};
+    // filter counts that are not multiples of 8 (TMA needs 16-byte row
+    // pitches): the filters are staged into a copy with a padded pitch
+    std::int64_t k_ld{0};
+    std::size_t f_stage_off{0};
     int ksteps{4};
     int box[3]{};  // image TMA box {w*n, h, c}
 };
@@ -411,8 +415,6 @@ ConvPlan conv_plan(const ConvInput& in, const ConvTuning& t) {
         throw unsupported_error("tensor-core conv family: W * N must fit in 32 bits");
     if (t.k_l < 16 || t.k_l > 256 || t.k_l % 16 != 0)
         throw unsupported_error("tensor-core conv family: k_l must be a multiple of 16 in [16, 256] (UMMA_N)");
-    if (in.k_filters % 8 != 0)
-        throw unsupported_error("tensor-core conv family: the filter count must be a multiple of 8 (TMA row pitch)");
     if (t.c_l != 1) throw unsupported_error("tensor-core conv family: c_l must be 1");
     if (t.c_s > 2) throw unsupported_error("tensor-core conv family: c_s (TMEM accumulator buffers) must be 1 or 2");
     if (t.u != 16 && t.u != 32 && t.u != 64 && t.u != 128)
@@ -506,6 +508,12 @@ ConvPlan conv_plan(const ConvInput& in, const ConvTuning& t) {
         pl.flag_bytes = (std::size_t(tiles_sp) * p.tiles_k * std::size_t(p.nz - 1) * 8 + 255) / 256 * 256;
         pl.ws_bytes = dev::kSplitCounterBytes + pl.flag_bytes + std::size_t(p.nz - 1) * std::size_t(in.k_filters) * std::size_t(pqn) * 4;
     }
+    pl.k_ld = (in.k_filters + 7) / 8 * 8;
+    if (pl.k_ld != in.k_filters) {
+        if (pl.ws_bytes == 0) pl.ws_bytes = dev::kSplitCounterBytes;
+        pl.f_stage_off = (pl.ws_bytes + 255) / 256 * 256;
+        pl.ws_bytes = pl.f_stage_off + std::size_t(crs) * std::size_t(pl.k_ld) * es;
+    }
     return pl;
 }
 
@@ -527,10 +535,18 @@ void conv(const ConvInput& in, const ConvTuning& t, const void* images, const vo
         throw unsupported_error("tensor-core conv family: image and filter pointers must be 16-byte aligned");
     if (const char* d = std::getenv("KTUNE_TC_DEBUG")) p.dbg = reinterpret_cast<long long*>(std::strtoull(d, nullptr, 0));
     p.out = static_cast<float*>(outputs);
+    if (pl.ws_bytes > 0 && (ws == nullptr || ws_bytes < pl.ws_bytes))
+        throw workspace_error("workspace of " + std::to_string(ws_bytes) + " bytes is smaller than the " +
+                              std::to_string(pl.ws_bytes) + " bytes this tuning needs");
+    if (pl.k_ld != in.k_filters) {
+        void* dst = static_cast<unsigned char*>(ws) + pl.f_stage_off;
+        dev::check(cudaMemcpy2DAsync(dst, std::size_t(pl.k_ld) * 2, filters, std::size_t(in.k_filters) * 2,
+                                     std::size_t(in.k_filters) * 2, std::size_t(in.c * in.r * in.s),
+                                     cudaMemcpyDeviceToDevice, stream),
+                   "stage filters");
+        filters = dst;
+    }
     if (p.nz > 1) {
-        if (ws == nullptr || ws_bytes < pl.ws_bytes)
-            throw workspace_error("workspace of " + std::to_string(ws_bytes) + " bytes is smaller than the " +
-                                  std::to_string(pl.ws_bytes) + " bytes this tuning needs");
         // past the SIMT family's zeroed counter region (kernels.hpp)
         p.flags = reinterpret_cast<unsigned long long*>(static_cast<unsigned char*>(ws) + dev::kSplitCounterBytes);
         p.ws = reinterpret_cast<float*>(static_cast<unsigned char*>(ws) + dev::kSplitCounterBytes + pl.flag_bytes);
@@ -541,7 +557,7 @@ void conv(const ConvInput& in, const ConvTuning& t, const void* images, const vo
     CUtensorMap mi = make_map_nd(images, in.dtype, 3, idims, pl.box, 128);
     const std::int64_t fdims[3] = {in.k_filters, in.r * in.s, in.c};
     const int fbox[3] = {p.b_sw / 2, 1, p.bk};
-    CUtensorMap mf = make_map_nd(filters, in.dtype, 3, fdims, fbox, p.b_sw);
+    CUtensorMap mf = make_map_nd(filters, in.dtype, 3, fdims, fbox, p.b_sw, pl.k_ld);
     using ktune_dev::tc::umma_conv_kernel;
     static const void* const kernels[4] = {
         reinterpret_cast<const void*>(&umma_conv_kernel<1>), reinterpret_cast<const void*>(&umma_conv_kernel<2>),

@@ -142,3 +142,12 @@ def test_launchability_rules(cuda):
     i2, f2 = operands(bad, 0)
     with pytest.raises(K.Unsupported, match="multiple of 8"):
         K.execute_conv(bad, T(64, 1, 8, 16, 64), i2.cuda(), f2.cuda())
+
+
+@pytest.mark.parametrize("k", [174, 87, 20])
+def test_filter_counts_not_multiple_of_8_staged(cuda, k):
+    """DeepBench speaker conv11/12 (K = 174 / 87): the filter tensor is staged
+    into a copy with a 16-byte row pitch (execute_conv runs any shape)."""
+    inp = K.ConvInput(16, 8, 8, k, 32, 3, 3, "bf16")
+    got, ref = run(inp, T(64, 1, 8, 16, 64))
+    assert O.max_rel_error(got, ref) < tol(32 * 9)
