@@ -472,7 +472,12 @@ TmaLaunch tma_geometry(const GemmInput& in, const Plan& pl, Mode mode, const voi
     {
         const std::int64_t blocks_total = std::int64_t(pl.col_tiles) * pl.row_tiles * p.nz;
         const std::int64_t per_sm = std::max<std::int64_t>(1, ceil_div(blocks_total, device_sm_count()));
-        g.n_producers = per_sm <= 2 ? std::clamp(boxes_per_step, 1, 4) : 1;
+        // measured (bench protocol): extra producers never paid for the SIMT
+        // tiles of the benchmark shapes (2560x16x2560: 4-5 blocks/SM; 512^3:
+        // 2 blocks/SM, 9.4 -> 7.0 TFLOP/s with 2), so one unless asked for
+        (void)per_sm;
+        (void)boxes_per_step;
+        g.n_producers = 1;
     }
     if (const char* e = std::getenv("KTUNE_SIMT_PRODUCERS")) g.n_producers = std::clamp(std::atoi(e), 1, 4);
     tl.threads = (g.producer_warp + g.n_producers) * 32;

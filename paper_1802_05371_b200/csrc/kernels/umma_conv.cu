@@ -92,7 +92,13 @@ __device__ __forceinline__ void conv_probe(const ConvTcParams& p, int i, int slo
     p.dbg[i * 4 + slot] = (long long)t;
 }
 
-constexpr int kConvThreads = 192;
+// warps 0..2: TMA producers (a TMA issue occupies its warp for a few hundred
+// cycles; the boxes of a stage are dealt round-robin), warp 3: MMA issuer,
+// warps 4..7: epilogue (TMEM lane quarters 0..3)
+constexpr int kConvProducers = 3;
+constexpr int kConvMmaWarp = 3;
+constexpr int kConvEpi0 = 128;
+constexpr int kConvThreads = 256;
 
 struct ConvUnit {
     int p0, q0, n0, k0, g, tile;
@@ -139,7 +145,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
-            mbar_init(full + s, 1);
+            mbar_init(full + s, kConvProducers);  // one arrive.expect_tx per producer warp
             mbar_init(empty + s, 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -150,7 +156,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&tma_i)) : "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&tma_f)) : "memory");
     }
-    if (warp == 1) {
+    if (warp == kConvMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
                      "r"(p.tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -161,16 +167,18 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const unsigned tmem_base = *tmem_slot;
     pdl_wait();  // setup above overlaps the previous kernel; global work starts here
 
-    if (warp == 0) {
-        // ---------------- TMA producer ----------------
-        // One warp walks every k-block of every unit in series, so its loop
-        // bounds the CTA's issue rate: the (tap, channel block) position
-        // advances incrementally (no divisions per k-block) and the per-unit
-        // box origins are computed once per unit.
+    if (warp < kConvProducers) {
+        // ---------------- TMA producers ----------------
+        // Each producer warp walks every k-block of every unit and issues the
+        // boxes b (two image atoms, then the filter boxes) with
+        // b % kConvProducers == warp; the (tap, channel block) position
+        // advances incrementally and the box origins are computed once per unit.
         int stage = 0;
         unsigned phase = 0;
         const int box_elems = p.b_sw / 2;
-        const unsigned tx_bytes = 2 * p.a_box_bytes + p.b_boxes * p.b_box_bytes;
+        const int nbox = 2 + p.b_boxes;
+        unsigned tx_bytes = 0;
+        for (int b = warp; b < nbox; b += kConvProducers) tx_bytes += b < 2 ? p.a_box_bytes : p.b_box_bytes;
         const int Nb = p.Nb, S = p.S, bk = p.bk, cblocks = p.cblocks, b_boxes = p.b_boxes;
         const unsigned a_tile = p.a_tile_bytes, a_box_stride = p.a_box_stride, b_box_stride = p.b_box_stride;
         int dbg_i = 0;
@@ -187,17 +195,20 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             int r = rs / S, sx = rs - r * S;
             for (int kb = kb_begin; kb < kb_end; ++kb, ++dbg_i) {
                 mbar_wait(empty + stage, phase ^ 1u);
-                if (lane == 0) conv_probe(p, dbg_i, 0);
+                if (lane == 0 && warp == 0) conv_probe(p, dbg_i, 0);
                 if (elect_one()) {
                     const int c0 = cb * bk;
                     unsigned char* sa = smem + std::size_t(stage) * stage_bytes;
                     unsigned char* sb = sa + a_tile;
                     mbar_expect_tx(full + stage, tx_bytes);
-                    tma_load_3d(sa, &tma_i, full + stage, ax0 + sx * Nb, ah0 + r, c0);
-                    tma_load_3d(sa + a_box_stride, &tma_i, full + stage, ax1 + sx * Nb, ah1 + r, c0);
-                    for (int j = 0; j < b_boxes; ++j)
-                        tma_load_3d(sb + j * b_box_stride, &tma_f, full + stage, w.k0 + j * box_elems, rs, c0);
-                    conv_probe(p, dbg_i, 2);
+                    for (int b = warp; b < 2 + b_boxes; b += kConvProducers) {
+                        if (b == 0) tma_load_3d(sa, &tma_i, full + stage, ax0 + sx * Nb, ah0 + r, c0);
+                        else if (b == 1) tma_load_3d(sa + a_box_stride, &tma_i, full + stage, ax1 + sx * Nb, ah1 + r, c0);
+                        else
+                            tma_load_3d(sb + (b - 2) * b_box_stride, &tma_f, full + stage, w.k0 + (b - 2) * box_elems,
+                                        rs, c0);
+                    }
+                    if (warp == 0) conv_probe(p, dbg_i, 2);
                 }
                 __syncwarp();
                 if (++cb == cblocks) {
@@ -214,7 +225,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == kConvMmaWarp) {
         // ---------------- MMA issuer ----------------
         int stage = 0;
         unsigned phase = 0;
@@ -278,9 +289,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             const long long pix = ((long long)(w.p0 + pp) * p.Q + (w.q0 + qq)) * p.Nb + (w.n0 + nn);
             mbar_wait(acc_full + acc, acc_phase);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            if (threadIdx.x == 64) conv_probe(p, 60 + (u / gridDim.x) % 4, 3);
+            if (threadIdx.x == kConvEpi0) conv_probe(p, 60 + (u / gridDim.x) % 4, 3);
             if (last && p.nz > 1) {
-                for (int gg = threadIdx.x - 64; gg < p.nz - 1; gg += 128) {
+                for (int gg = threadIdx.x - kConvEpi0; gg < p.nz - 1; gg += 128) {
                     unsigned long long* flag = p.flags + std::int64_t(gg) * tiles + w.tile;
                     unsigned long long v;
                     while (true) {
@@ -349,7 +360,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 // bar.sync orders the 128 threads' partial stores before one
                 // thread's cumulative gpu-scope release (no per-thread fence)
                 asm volatile("bar.sync 1, 128;\n" ::: "memory");
-                if (threadIdx.x == 64) {
+                if (threadIdx.x == kConvEpi0) {
                     unsigned long long* flag = p.flags + std::int64_t(w.g) * tiles + w.tile;
                     asm volatile("fence.acq_rel.gpu;\nst.release.gpu.global.u64 [%0], %1;\n" ::"l"(flag), "l"(p.token)
                                  : "memory");
@@ -363,7 +374,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
-    if (warp == 1) {
+    if (warp == kConvMmaWarp) {
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(p.tmem_cols));
     }
