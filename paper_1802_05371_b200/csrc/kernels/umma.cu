@@ -51,6 +51,7 @@ struct TcParams {
     int stages;
     int kb_total;                 // k-blocks per tile
     int streamk;                  // k_g > 1: balanced contiguous (tile, k-block) ranges per CTA
+    int csplit;                   // > 1: the k_g slices of a tile are one cluster, reduced through DSMEM
     long long total_it;           // tiles * kb_total (stream-K iteration space)
     int smax, gmax;               // stream-K: max segments per tile, max fold groups per tile
     int a_kmajor, b_kmajor;
@@ -155,6 +156,16 @@ __device__ __forceinline__ int cfind(long long i, long long T, int G) {
 template <class F>
 __device__ __forceinline__ void for_each_seg(const TcParams& p, int cta, int ncta, F&& fn) {
     const int tiles = p.tiles_m * p.tiles_n;
+    if (p.csplit > 1) {
+        // cluster split: cluster c owns tile c, rank r its r-th contiguous K share
+        const int C = p.csplit, t = cta / C, r = cta - t * C;
+        if (t < tiles) {
+            const Unit w = unit_of(p, t);
+            fn(Seg{w.m0, w.n0, w.tile, int((long long)r * p.kb_total / C), int((long long)(r + 1) * p.kb_total / C), r,
+                   C});
+        }
+        return;
+    }
     if (!p.streamk) {
         for (int t = cta; t < tiles; t += ncta) {
             const Unit w = unit_of(p, t);
@@ -397,7 +408,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // of warp quarter q (the upper 16 lanes of each quarter unused)
             const int row = p.bm == 64 ? w.m0 + quarter * 16 + lane : w.m0 + int(rank) * 128 + quarter * 32 + lane;
             const bool row_ok = row < p.M && (p.bm == 64 ? lane < 16 : true);
-            const bool split = w.S > 1;
+            const bool csplit = p.csplit > 1;
+            const bool split = w.S > 1 && !csplit;
             mbar_wait(acc_full + acc, acc_phase);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             if (threadIdx.x == kEpi0 && first) probe(p, 5);
@@ -418,6 +430,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
                     if constexpr (PAIR) mbar_arrive_cluster(acc_empty_leader0 + unsigned(acc) * 8u);
                     else mbar_arrive(acc_empty + acc);
+                }
+                if (csplit) {
+                    if (p.bm == 64 && lane >= 16) continue;
+                    // this slice's partial row into its own shared memory (the
+                    // pipeline ring is idle: every k-block of the slice has been
+                    // consumed); an empty slice contributes zeros
+                    float* red = reinterpret_cast<float*>(smem) + (row - w.m0) * p.bn + c0;
+                    const bool empty_slice = w.kb1 == w.kb0;
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4)
+                        if (i < chunk)
+                            *reinterpret_cast<float4*>(red + i) = empty_slice ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                                                              : make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                    continue;
                 }
                 if (!row_ok) continue;
                 const std::int64_t base = std::int64_t(row) * p.N + w.n0 + c0;
@@ -524,7 +550,65 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     if constexpr (PAIR) cluster_sync();  // the peer's MMAs / smem reads are done before either CTA frees
-    else __syncthreads();
+    else if (p.csplit > 1) {
+        // cluster split-K: every slice's partial tile sits in its CTA's shared
+        // memory; after one cluster barrier every rank reads its share of the
+        // tile from all slices through DSMEM, folds it in rank order
+        // (((0 + s_0) + s_1) + ...) and writes C
+        if (threadIdx.x == kEpi0) probe(p, 6);
+        cluster_sync();
+        if (threadIdx.x == 0 && p.dbg != nullptr) {  // per-CTA: every slice's partial is in place
+            unsigned long long tt;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+            p.dbg[1024 + blockIdx.x * 4 + 2] = (long long)tt;
+        }
+        // rank r folds quads [r*Q/C, (r+1)*Q/C) of the tile with all its
+        // threads; every quad is summed over the slices in rank order
+        const int crank = int(cluster_ctarank());
+        const int C = p.csplit;
+        const int t = int(blockIdx.x) / C;
+        if (t < p.tiles_m * p.tiles_n) {
+            const Unit w = unit_of(p, t);
+            const int qpr = p.bn / 4, Q = p.bm * qpr;
+            const int q1 = (crank + 1) * Q / C;
+            const unsigned sbase = smem_u32(smem);
+            for (int q = crank * Q / C + int(threadIdx.x); q < q1; q += kThreads) {
+                const int lrow = q / qpr, c4 = q - lrow * qpr;
+                const int row = w.m0 + lrow, col = w.n0 + c4 * 4;
+                if (row >= p.M || col >= p.N) continue;
+                float4 x[8];
+                unsigned ad[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) ad[r] = r < C ? mapa_shared(sbase + unsigned(q) * 16u, unsigned(r)) : 0u;
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+                    if (r < C)
+                        asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                                     : "=f"(x[r].x), "=f"(x[r].y), "=f"(x[r].z), "=f"(x[r].w)
+                                     : "r"(ad[r]));
+                float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+                    if (r < C) {
+                        acc4.x = __fadd_rn(acc4.x, x[r].x);
+                        acc4.y = __fadd_rn(acc4.y, x[r].y);
+                        acc4.z = __fadd_rn(acc4.z, x[r].z);
+                        acc4.w = __fadd_rn(acc4.w, x[r].w);
+                    }
+                float* dst = p.C + std::int64_t(row) * p.N + col;
+                if (col + 4 <= p.N && (reinterpret_cast<std::uintptr_t>(dst) & 15) == 0) {
+                    *reinterpret_cast<float4*>(dst) = acc4;
+                } else {
+                    const float vv[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
+                    for (int i = 0; i < 4 && col + i < p.N; ++i) dst[i] = vv[i];
+                }
+            }
+        }
+        // execution-only barrier: the peers' shared memory stays alive until
+        // every rank has read it (the reads completed into registers above);
+        // no release, so the C stores need not be acknowledged first
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;\n" ::: "memory");
+    } else __syncthreads();
     if (threadIdx.x == 0) probe(p, 7);
     if (threadIdx.x == 0 && p.dbg != nullptr) {
         unsigned long long t;
@@ -716,9 +800,34 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     if (tiles > 0x7fffffff) throw unsupported_error("too many output tiles for one launch");
     const std::int64_t slots = pl.pair ? num_sms() / 2 : num_sms();
     p.streamk = t.k_g > 1 ? 1 : 0;
+    p.csplit = 0;
+    // cluster split: when at least two slices of every tile fit the SMs at
+    // once, each tile is one cluster of C CTAs -- the largest power of two
+    // <= min(k_g, 8) whose clusters are all resident together (like
+    // stream-K, k_g caps the workers at what the SMs hold) -- and the slices
+    // are reduced through distributed shared memory: no global partials,
+    // atomics or fold pass.  Otherwise stream-K.  Resident clusters: pairs
+    // fill every SM; clusters of 4 strand a few SMs per GPC (132 of 148 CTAs
+    // measured); 8 is held to 3/4 of the SMs.  Odd sizes pack GPCs badly
+    // (k_g = 8 as 7-CTA clusters ran a second wave: 14.4 us vs 8.4 us).
+    {
+        const std::int64_t sms = num_sms();
+        int C = 0;
+        for (int c = 2; c <= 8 && c <= t.k_g && c <= p.kb_total; c *= 2) {
+            const std::int64_t cap = c == 2 ? sms : (c == 4 ? sms * 132 / 148 : sms * 3 / 4);
+            if (tiles * c <= cap) C = c;
+        }
+        if (!pl.pair && t.k_g > 1 && C >= 2 &&
+            std::size_t(p.bm) * p.bn * 4 <= std::size_t(p.stages) * (std::size_t(p.a_tile_bytes) + p.b_tile_bytes) &&
+            std::getenv("KTUNE_TC_NO_CSPLIT") == nullptr) {
+            p.csplit = C;
+            p.streamk = 0;
+        }
+    }
     p.total_it = tiles * p.kb_total;
     std::int64_t G = p.streamk ? std::min<std::int64_t>({slots, tiles * t.k_g, p.total_it})
                                : std::min<std::int64_t>(slots, tiles);
+    if (p.csplit > 1) G = tiles * p.csplit;
     G = std::max<std::int64_t>(G, 1);
     pl.grid = dim3(unsigned(pl.pair ? 2 * G : G), 1, 1);
     p.smax = 1;
@@ -802,8 +911,14 @@ std::size_t gemm_workspace_bytes(const GemmInput& in, const GemmTuning& t) { ret
 
 dev::LaunchInfo gemm_launch_info(const GemmInput& in, const GemmTuning& t) {
     TcPlan pl = tc_plan(in, t);
+    // the family names the K-split schedule the plan chose
+    const char* fam = pl.p.csplit == 2   ? "tcgen05-cluster2"
+                      : pl.p.csplit == 4 ? "tcgen05-cluster4"
+                      : pl.p.csplit == 8 ? "tcgen05-cluster8"
+                      : pl.p.streamk     ? (pl.pair ? "tcgen05-pair-streamk" : "tcgen05-streamk")
+                                         : (pl.pair ? "tcgen05-pair" : "tcgen05");
     return dev::LaunchInfo{ktune_dev::tc::kThreads, pl.smem, int(pl.grid.x), int(pl.grid.y), int(pl.grid.z), false,
-                           "tcgen05"};
+                           fam};
 }
 
 void gemm(const GemmInput& in, const GemmTuning& t, const void* a, const void* b, void* c, void* ws,
@@ -872,8 +987,8 @@ void gemm(const GemmInput& in, const GemmTuning& t, const void* a, const void* b
         }
     }
     void* args[] = {&ma, &mb, &p};
-    dev::launch(kern, pl.grid, dim3(ktune_dev::tc::kThreads), args, pl.smem, stream, pl.pair ? 2 : 1,
-                pl.pair ? "umma pair launch" : "umma launch");
+    dev::launch(kern, pl.grid, dim3(ktune_dev::tc::kThreads), args, pl.smem, stream,
+                pl.pair ? 2 : (p.csplit > 1 ? p.csplit : 1), pl.pair ? "umma pair launch" : "umma launch");
 }
 
 }  // namespace umma
