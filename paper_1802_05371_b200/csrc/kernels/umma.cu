@@ -52,6 +52,7 @@ struct TcParams {
     int kb_total;                 // k-blocks per tile
     int streamk;                  // k_g > 1: balanced contiguous (tile, k-block) ranges per CTA
     int csplit;                   // > 1: the k_g slices of a tile are one cluster, reduced through DSMEM
+    int deal_rotate;              // deal TMA boxes round-robin across stages (else box b -> warp b % kProducers)
     long long total_it;           // tiles * kb_total (stream-K iteration space)
     int smax, gmax;               // stream-K: max segments per tile, max fold groups per tile
     int a_kmajor, b_kmajor;
@@ -263,16 +264,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp < kProducers) {
         // ---------------- TMA producers (each warp loops, one lane issues) ----------------
-        // Box b of a stage (A boxes first, then B boxes) is issued by warp
-        // b % kProducers; every producer arrives on the stage's full barrier
-        // with the bytes of its own boxes (x2 for a pair: the follower issues
-        // the same boxes onto the leader's barrier).
+        // Boxes are dealt round-robin over the producer warps across stages
+        // (box b of the stage whose first box has running index s goes to
+        // warp (s + b) % kProducers): a TMA issue occupies its warp for a few
+        // hundred cycles, so with fewer boxes per stage than producers every
+        // warp still issues every few stages.  Every producer arrives on each
+        // stage's full barrier with the bytes of its own boxes, possibly none
+        // (x2 for a pair: the follower issues the same boxes onto the
+        // leader's barrier).
         int stage = 0;
         unsigned phase = 0;
         const int a_box_elems = p.a_sw / p.esize, b_box_elems = p.b_sw / p.esize;
         const int nbox = p.a_boxes + p.b_boxes;
-        unsigned my_bytes = 0;
-        for (int b = warp; b < nbox; b += kProducers) my_bytes += b < p.a_boxes ? p.a_box_bytes : p.b_box_bytes;
+        int b_first = warp;  // this warp's first box of the current stage
+        const int nbox_mod = p.deal_rotate ? nbox % kProducers : 0;
         const int a_row = PAIR ? int(rank) * 128 : 0;                 // this CTA's rows of the tile
         const int b_col = PAIR ? int(rank) * (p.bn / 2) : 0;          // this CTA's half of the columns
         int dbg_i = 0;
@@ -286,6 +291,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     first = false;
                     unsigned char* sa = smem + std::size_t(stage) * stage_bytes;
                     unsigned char* sb = sa + p.a_tile_bytes;
+                    unsigned my_bytes = 0;
+                    for (int b = b_first; b < nbox; b += kProducers)
+                        my_bytes += b < p.a_boxes ? p.a_box_bytes : p.b_box_bytes;
                     const int k0 = kb * p.bk;
                     const int m0 = w.m0 + a_row, n0 = w.n0 + b_col;
                     if constexpr (PAIR) {
@@ -293,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         // the follower's bytes may land before the leader's expect_tx:
                         // the phase cannot complete until the leader's producers arrive
                         if (leader) mbar_expect_tx(full + stage, 2 * my_bytes);
-                        for (int b = warp; b < nbox; b += kProducers) {
+                        for (int b = b_first; b < nbox; b += kProducers) {
                             if (b < p.a_boxes) {
                                 const int j = b;
                                 if (p.a_kmajor) tma_load_2d_pair(sa + j * p.a_box_stride, &tma_a, bar, k0 + j * a_box_elems, m0);
@@ -307,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (warp == 0) probe_kb(p, dbg_i, 1);
                     } else {
                         mbar_expect_tx(full + stage, my_bytes);
-                        for (int b = warp; b < nbox; b += kProducers) {
+                        for (int b = b_first; b < nbox; b += kProducers) {
                             if (b < p.a_boxes) {
                                 const int j = b;
                                 if (p.a_kmajor)
@@ -325,6 +333,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 __syncwarp();
+                b_first -= nbox_mod;  // the next stage's boxes start nbox later in the deal
+                if (b_first < 0) b_first += kProducers;
                 if (++stage == p.stages) {
                     stage = 0;
                     phase ^= 1u;
@@ -801,8 +811,9 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     const std::int64_t slots = pl.pair ? num_sms() / 2 : num_sms();
     p.streamk = t.k_g > 1 ? 1 : 0;
     p.csplit = 0;
-    // cluster split: when at least two slices of every tile fit the SMs at
-    // once, each tile is one cluster of C CTAs -- the largest power of two
+    p.deal_rotate = std::getenv("KTUNE_TC_STATIC_DEAL") == nullptr ? 1 : 0;
+    // cluster split: when k_g <= 8 and at least two slices of every tile fit
+    // the SMs at once, each tile is one cluster of C CTAs -- the largest power of two
     // <= min(k_g, 8) whose clusters are all resident together (like
     // stream-K, k_g caps the workers at what the SMs hold) -- and the slices
     // are reduced through distributed shared memory: no global partials,
@@ -810,6 +821,8 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
     // fill every SM; clusters of 4 strand a few SMs per GPC (132 of 148 CTAs
     // measured); 8 is held to 3/4 of the SMs.  Odd sizes pack GPCs badly
     // (k_g = 8 as 7-CTA clusters ran a second wave: 14.4 us vs 8.4 us).
+    // k_g > 8 asks for more workers than a cluster holds: stream-K (ICA
+    // 32x32x60000 at k_g = 32: 64 stream-K CTAs 13 us, 16 clustered 27 us).
     {
         const std::int64_t sms = num_sms();
         int C = 0;
@@ -817,7 +830,7 @@ TcPlan tc_plan(const GemmInput& in, const GemmTuning& t) {
             const std::int64_t cap = c == 2 ? sms : (c == 4 ? sms * 132 / 148 : sms * 3 / 4);
             if (tiles * c <= cap) C = c;
         }
-        if (!pl.pair && t.k_g > 1 && C >= 2 &&
+        if (!pl.pair && t.k_g > 1 && t.k_g <= 8 && C >= 2 &&
             std::size_t(p.bm) * p.bn * 4 <= std::size_t(p.stages) * (std::size_t(p.a_tile_bytes) + p.b_tile_bytes) &&
             std::getenv("KTUNE_TC_NO_CSPLIT") == nullptr) {
             p.csplit = C;

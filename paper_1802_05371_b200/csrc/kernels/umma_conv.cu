@@ -169,16 +169,18 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 
     if (warp < kConvProducers) {
         // ---------------- TMA producers ----------------
-        // Each producer warp walks every k-block of every unit and issues the
-        // boxes b (two image atoms, then the filter boxes) with
-        // b % kConvProducers == warp; the (tap, channel block) position
-        // advances incrementally and the box origins are computed once per unit.
+        // Each producer warp walks every k-block of every unit; the boxes (two
+        // image atoms, then the filter boxes) are dealt round-robin over the
+        // producer warps across stages, as in the GEMM (umma.cu), so every
+        // warp issues even when a stage has fewer boxes than producers.  The
+        // (tap, channel block) position advances incrementally and the box
+        // origins are computed once per unit.
         int stage = 0;
         unsigned phase = 0;
         const int box_elems = p.b_sw / 2;
         const int nbox = 2 + p.b_boxes;
-        unsigned tx_bytes = 0;
-        for (int b = warp; b < nbox; b += kConvProducers) tx_bytes += b < 2 ? p.a_box_bytes : p.b_box_bytes;
+        int b_first = warp;
+        const int nbox_mod = nbox % kConvProducers;
         const int Nb = p.Nb, S = p.S, bk = p.bk, cblocks = p.cblocks, b_boxes = p.b_boxes;
         const unsigned a_tile = p.a_tile_bytes, a_box_stride = p.a_box_stride, b_box_stride = p.b_box_stride;
         int dbg_i = 0;
@@ -200,8 +202,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     const int c0 = cb * bk;
                     unsigned char* sa = smem + std::size_t(stage) * stage_bytes;
                     unsigned char* sb = sa + a_tile;
+                    unsigned tx_bytes = 0;
+                    for (int b = b_first; b < nbox; b += kConvProducers)
+                        tx_bytes += b < 2 ? p.a_box_bytes : p.b_box_bytes;
                     mbar_expect_tx(full + stage, tx_bytes);
-                    for (int b = warp; b < 2 + b_boxes; b += kConvProducers) {
+                    for (int b = b_first; b < 2 + b_boxes; b += kConvProducers) {
                         if (b == 0) tma_load_3d(sa, &tma_i, full + stage, ax0 + sx * Nb, ah0 + r, c0);
                         else if (b == 1) tma_load_3d(sa + a_box_stride, &tma_i, full + stage, ax1 + sx * Nb, ah1 + r, c0);
                         else
@@ -211,6 +216,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     if (warp == 0) conv_probe(p, dbg_i, 2);
                 }
                 __syncwarp();
+                b_first -= nbox_mod;
+                if (b_first < 0) b_first += kConvProducers;
                 if (++cb == cblocks) {
                     cb = 0;
                     ++rs;

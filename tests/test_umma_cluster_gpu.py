@@ -1,14 +1,12 @@
-"""Cluster split-K of the tensor-core GEMM: when at least two K slices of
-every output tile fit the SMs at once, a tile is one thread-block cluster
-of C = 2/4/8 CTAs (a power of two <= k_g), each slice leaves its partial
+"""Cluster split-K of the tensor-core GEMM: when k_g <= 8 and at least two
+K slices of every output tile fit the SMs at once, a tile is one
+thread-block cluster of C = 2/4/8 CTAs (a power of two <= k_g), each slice leaves its partial
 tile in its own shared memory, and after one cluster barrier every rank
 folds its share of the tile over the slices in rank order through DSMEM
 (no global partials, counters or fold pass; no workspace).  Larger splits
 keep stream-K (test_umma_streamk_gpu.py).  Same contract as
 test_umma_gpu.py: quantised inputs, double reference, max(1e-4, 6e-8 K);
 bit-stable across runs and CUDA-graph replays."""
-import os
-
 import numpy as np
 import pytest
 import torch
@@ -41,6 +39,8 @@ def run_twice(inp, tv, seed=0):
     ((2560, 16, 2560, False, False), (8, 4, 128, 16, 64, 1, 1, 8), "tcgen05-cluster4"),
     # few tiles: clusters of 8
     ((192, 96, 4000, False, True), (8, 8, 128, 32, 64, 1, 1, 8), "tcgen05-cluster8"),
+    # k_g > 8 asks for more workers than one cluster holds: stream-K
+    ((32, 32, 60000, False, True), (8, 16, 64, 16, 128, 1, 1, 32), "tcgen05-streamk"),
     # too many tiles for two slices each: stream-K
     ((2560, 512, 2560, False, False), (8, 4, 128, 16, 64, 1, 1, 4), "tcgen05-streamk"),
 ])
