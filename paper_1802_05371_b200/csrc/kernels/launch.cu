@@ -154,7 +154,7 @@ int device_sm_count() {
 Plan plan_simt(std::int64_t rows, std::int64_t red, std::int64_t out_elems, std::int64_t col_tiles, int ml, int nl,
                int ms, int ns, int ks, int kl, int kg, int u, int esize, bool arm, bool brm,
                const std::function<int(int w, std::int64_t span_gcd)>& pick_va,
-               const std::function<int(int w, std::int64_t span_gcd)>& pick_vb) {
+               const std::function<int(int w, std::int64_t span_gcd)>& pick_vb, std::int64_t span_override = 0) {
     Plan pl;
     auto& p = pl.p;
     p.rows = rows;
@@ -172,7 +172,7 @@ Plan plan_simt(std::int64_t rows, std::int64_t red, std::int64_t out_elems, std:
     p.lw = ilog2(p.w);
     p.lml = ilog2(ml);
     p.lnl = ilog2(nl);
-    p.kg_span = ceil_div(red, kg);
+    p.kg_span = span_override > 0 ? span_override : ceil_div(red, kg);
     p.nz = int(ceil_div(red, p.kg_span));
     const std::int64_t span_gcd = slice_gcd_span(red, p.kg_span, p.nz, kl);
     const int va = pick_va(p.w, span_gcd), vb = pick_vb(p.w, span_gcd);
@@ -321,7 +321,46 @@ void bind_workspace(Plan& pl, void* ws, std::size_t ws_bytes) {
 
 // Pointers are only used for vector-width alignment (nullptr = assume the
 // 256-byte alignment of cudaMalloc, for workspace/launch-info queries).
-Plan gemm_plan(const GemmInput& in, const GemmTuning& t, const void* a = nullptr, const void* b = nullptr) {
+// FAST-mode wave balance of the k_g split.  A SIMT block's time is issue
+// bound and the blocks of one SM share its issue slots, so a launch lasts as
+// long as its most loaded SM: ceil(blocks / SMs) blocks of K / slices
+// columns each.  The tuple's k_g slices rarely divide evenly over 148 SMs
+// (2560x16x2560 at k_g = 8: 640 blocks, 4.3 per SM, the SMs with 5 finish
+// ~16 % after the rest), so FAST re-slices K into the count in [k_g, 2*k_g]
+// that minimises ceil(tiles * slices / SMs) / slices without putting more
+// blocks on an SM than the tuple's own grid does (residency: 2560x16x2560
+// at 9 slices 16.8 -> 16.0 us; at 10+ slices a sixth block per SM spilled
+// into a second wave, 18-45 us), with slice starts kept 16-byte aligned
+// (vector / TMA feeds).  The summation
+// order changes (FAST's contract: within 1e-5 of the reference), the tile
+// geometry does not; PARITY keeps the reference's k_g slices.
+// KTUNE_SIMT_NZ forces a slice count (measurement); KTUNE_SIMT_NO_BALANCE
+// keeps k_g.
+std::int64_t balanced_span(const GemmInput& in, const GemmTuning& t, int es) {
+    if (t.k_g < 2 || std::getenv("KTUNE_SIMT_NO_BALANCE") != nullptr) return 0;
+    const std::int64_t tiles = ceil_div(in.m, t.m_l) * ceil_div(in.n, t.n_l);
+    const std::int64_t sms = device_sm_count();
+    const std::int64_t vec = 16 / es;
+    auto span_of = [&](std::int64_t nz) { return ceil_div(ceil_div(in.k, nz), vec) * vec; };
+    if (const char* e = std::getenv("KTUNE_SIMT_NZ")) return span_of(std::max<std::int64_t>(1, std::atoll(e)));
+    std::int64_t best_nz = t.k_g;
+    const std::int64_t per_sm0 = ceil_div(tiles * t.k_g, sms);
+    double best = double(per_sm0) / double(t.k_g);
+    for (std::int64_t nz = t.k_g + 1; nz <= 2 * t.k_g; ++nz) {
+        const std::int64_t span = span_of(nz);
+        const std::int64_t real = ceil_div(in.k, span);  // slices after alignment
+        if (ceil_div(tiles * real, sms) > per_sm0) break;
+        const double cost = double(ceil_div(tiles * real, sms)) * double(span) / double(in.k);
+        if (cost < best * 0.98) {
+            best = cost;
+            best_nz = real;
+        }
+    }
+    return best_nz == t.k_g ? 0 : span_of(best_nz);
+}
+
+Plan gemm_plan(const GemmInput& in, const GemmTuning& t, const void* a = nullptr, const void* b = nullptr,
+               bool balance = false) {
     in.validate();
     t.validate();
     require_divisible(t.m_l, t.m_s, "m_l not divisible by m_s");
@@ -338,7 +377,7 @@ Plan gemm_plan(const GemmInput& in, const GemmTuning& t, const void* a = nullptr
         return brm ? vec_width(es, {in.k, span_gcd}, {b}, w) : vec_width(es, {in.n}, {b}, t.n_l);
     };
     Plan pl = plan_simt(in.m, in.k, in.m * in.n, ceil_div(in.n, t.n_l), t.m_l, t.n_l, t.m_s, t.n_s, t.k_s, t.k_l,
-                        t.k_g, t.u, es, arm, brm, va, vb);
+                        t.k_g, t.u, es, arm, brm, va, vb, balance ? balanced_span(in, t, es) : 0);
     // Precomputed chunk loader: every thread's chunks fit ktune_dev::kChunkMax
     // and every operand offset fits in 32 bits.
     auto chunks = [&](int lrows, int lv) {
@@ -377,6 +416,7 @@ Plan conv_plan(const ConvInput& in, const ConvTuning& t, const void* img = nullp
     const std::int64_t a_total = std::int64_t(pl.p.kl) << (pl.p.lml + pl.p.lw - pl.p.lva);
     pl.p.fast_ld = ceil_div(a_total, pl.threads) <= ktune_dev::kChunkMax &&
                    in.c * in.r * in.s * in.k_filters < (std::int64_t(1) << 31);
+    pl.p.gather_ld = std::getenv("KTUNE_SIMT_NO_GATHER") == nullptr ? 1 : 0;
     return pl;
 }
 
@@ -585,6 +625,19 @@ void launch_conv_t(const ConvInput& in, const ConvTuning& t, Plan& pl, Mode mode
     prob.nlb = t.n_l;
     prob.tiles_q = int(ceil_div(in.q, t.q_l));
     prob.tiles_n = int(ceil_div(in.n_batch, t.n_l));
+    prob.wn = std::int64_t(in.w()) * in.n_batch;
+    prob.hwn = std::int64_t(in.h()) * prob.wn;
+    {
+        // multiply-high division of the tap decomposition: exact while
+        // t * d < 2^32 for every reduction index t < C*R*S (see ConvProblem::off)
+        const std::uint64_t rs = std::uint64_t(in.r) * in.s, crs = std::uint64_t(in.c) * rs;
+        auto mul = [](std::uint64_t d) { return d <= 1 ? 0u : unsigned(((std::uint64_t(1) << 32) + d - 1) / d); };
+        prob.magic = crs * rs < (std::uint64_t(1) << 32) ? 1u : 0u;
+        prob.m_rs = mul(rs);
+        prob.m_s = mul(std::uint64_t(in.s));
+        prob.one_rs = rs == 1 ? 0xFFFFFFFFu : 0u;
+        prob.one_s = in.s == 1 ? 0xFFFFFFFFu : 0u;
+    }
     pl.p.out = out;
     const void* k = pick(true, in.dtype, mode, pl);
     prepare(k, pl.smem);
@@ -596,7 +649,8 @@ void launch_conv_t(const ConvInput& in, const ConvTuning& t, Plan& pl, Mode mode
 
 std::size_t gemm_workspace_bytes(const GemmInput& in, const GemmTuning& t) {
     if (is_tensor_core_dtype(in.dtype)) return umma::gemm_workspace_bytes(in, t);
-    return gemm_plan(in, t).ws_bytes;
+    // either mode's plan fits (FAST may re-slice K: balanced_span)
+    return std::max(gemm_plan(in, t).ws_bytes, gemm_plan(in, t, nullptr, nullptr, true).ws_bytes);
 }
 
 std::size_t conv_workspace_bytes(const ConvInput& in, const ConvTuning& t) {
@@ -610,7 +664,7 @@ void gemm(const GemmInput& in, const GemmTuning& t, Mode mode, const void* a, co
         umma::gemm(in, t, a, b, c, ws, ws_bytes, stream);
         return;
     }
-    Plan pl = gemm_plan(in, t, a, b);
+    Plan pl = gemm_plan(in, t, a, b, mode == Mode::fast);
     bind_workspace(pl, ws, ws_bytes);
     pick(false, in.dtype, mode, pl);  // resolves pl.generic
     TmaLaunch tl = tma_geometry(in, pl, mode, a, b);
@@ -633,7 +687,7 @@ void conv(const ConvInput& in, const ConvTuning& t, Mode mode, const void* image
 
 LaunchInfo gemm_launch_info(const GemmInput& in, const GemmTuning& t, Mode mode) {
     if (is_tensor_core_dtype(in.dtype)) return umma::gemm_launch_info(in, t);
-    Plan pl = gemm_plan(in, t);
+    Plan pl = gemm_plan(in, t, nullptr, nullptr, mode == Mode::fast);
     pick(false, in.dtype, mode, pl);
     // nullptr operands: assume cudaMalloc alignment
     static const float aligned_probe[4] alignas(16) = {};

@@ -58,6 +58,7 @@ struct SimtParams {
     unsigned long long* flags;  // [nz-1][tiles] publication tokens
     unsigned long long token;   // unique per launch (never 0)
     int fast_ld;                // affine problems: per-thread chunk state precomputed (see ChunkLd)
+    int gather_ld;              // CONV: per-thread gather chunk state precomputed (see GatherLd)
     long long* dbg;             // optional timeline probe (KTUNE_SIMT_DEBUG): blocks x = 0, y in {0, 1}
 };
 
@@ -137,6 +138,11 @@ struct ConvProblem {
     std::int64_t Nb, P, Q, K, C, R, S, H, W;
     int pl, ql, nlb;              // spatial block tile
     int tiles_q, tiles_n;         // column-tile grid decomposition
+    std::int64_t hwn, wn;         // image strides of a channel and of a row
+    // t / (R*S) and rem / S as multiply-high by ceil(2^32 / d) (exact while
+    // t * R*S < 2^32, host-checked; magic = 0 keeps the divisions); d = 1
+    // has no 32-bit multiplier and passes n through the mask instead
+    unsigned magic, m_rs, m_s, one_rs, one_s;
     // The host only vectorises the gather when n-runs are whole chunks, so a
     // chunk is entirely valid or entirely outside the tensor.
     __device__ int b_cols_valid(std::int64_t base, int v) const { return base < 0 ? 0 : v; }
@@ -148,11 +154,20 @@ struct ConvProblem {
     // ones dominated the gather loader's instruction count.
     __device__ std::int64_t off(std::int64_t t) const {
         const unsigned tt = unsigned(t), rs = unsigned(R * S), ss = unsigned(S);
-        const unsigned c = tt / rs;
+        unsigned c, r;
+        if (magic) {
+            c = __umulhi(tt, m_rs) + (tt & one_rs);
+        } else {
+            c = tt / rs;
+        }
         const unsigned rem = tt - c * rs;
-        const unsigned r = rem / ss;
+        if (magic) {
+            r = __umulhi(rem, m_s) + (rem & one_s);
+        } else {
+            r = rem / ss;
+        }
         const unsigned s = rem - r * ss;
-        return (std::int64_t(c) * H + r) * W * Nb + std::int64_t(s) * Nb;
+        return std::int64_t(c) * hwn + std::int64_t(r) * wn + std::int64_t(s) * Nb;
     }
     __device__ const T* b_addr(std::int64_t t, std::int64_t base) const { return img + base + off(t); }
     __device__ void column(int ct, int x, std::int64_t& base, std::int64_t& out_col) const {
@@ -503,6 +518,63 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads : LaunchCap<MS_, NS_, 
             }
         }
     }
+    // ---- precomputed gather state (CONV image operand) ------------------------
+    // Per chunk: its column base (or < 0 outside the tensor), first reduction
+    // index and the columns left in its group; a step only adds st*w and
+    // decomposes the tap (ConvProblem::off).  The reduction index of the
+    // gather fits in 32 bits (host-checked).
+    struct GatherLd {
+        std::int64_t base;
+        int t0, lim, dst;
+    };
+    GatherLd cgs[kChunkMax];
+    int ncg = 0;
+    bool gather_fast = false;
+    if constexpr (!Prob::kAffine) {
+        const int lchunks = p.lnl + p.lw - p.lvb;
+        const int total = p.kl << lchunks;
+        if (p.gather_ld && (total + nthreads - 1) / nthreads <= kChunkMax) {
+            gather_fast = true;
+            const int inner = BRM ? (p.lw - p.lvb) : (p.lnl - p.lvb);
+            ncg = max(0, (total - tid + nthreads - 1) / nthreads);
+#pragma unroll
+            for (int i = 0; i < kChunkMax; ++i) {
+                if (i >= ncg) break;
+                const int e = tid + i * nthreads;
+                const int gx = e >> lchunks;
+                const int c = e & ((1 << lchunks) - 1);
+                const int outer = c >> inner;
+                const int in = (c & ((1 << inner) - 1)) << p.lvb;
+                const int xx = BRM ? outer : in;
+                const int kk = BRM ? in : outer;
+                const std::int64_t glo = min(s_hi, s_lo + gx * kl_span);
+                const std::int64_t ghi = min(s_hi, glo + kl_span);
+                cgs[i].base = col_base[xx];
+                cgs[i].t0 = int(glo + kk);
+                cgs[i].lim = int(ghi - (glo + kk));
+                cgs[i].dst = gx * p.b_group + (BRM ? xx * p.b_ld + kk : kk * p.b_ld + xx);
+            }
+        }
+    }
+    auto load_gather = [&]<int BYTES>(std::int64_t st, T* dst) {
+        if constexpr (!Prob::kAffine) {
+            constexpr int V = BYTES / int(sizeof(T));
+            const int dk = int(st) * p.w;
+            const T* dummy = reinterpret_cast<const T*>(p.out);
+#pragma unroll
+            for (int i = 0; i < kChunkMax; ++i) {
+                if (i < ncg) {
+                    const int r = cgs[i].lim - dk;
+                    const std::int64_t base = cgs[i].base;
+                    int n;
+                    if constexpr (BRM) n = base >= 0 ? min(max(r, 0), V) : 0;
+                    else n = r > 0 ? prob.b_cols_valid(base, V) : 0;
+                    const T* src = n > 0 ? prob.b_addr(cgs[i].t0 + dk, base) : dummy;
+                    cp_async_zfill<BYTES>(dst + cgs[i].dst, src, n * int(sizeof(T)));
+                }
+            }
+        }
+    };
     auto load_fast_a = [&]<int BA>(std::int64_t st, T* dst) {
         if constexpr (Prob::kAffineA) {
             const int dk = int(st) * p.w;
@@ -564,6 +636,14 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads : LaunchCap<MS_, NS_, 
                 case 8: load_a.template operator()<8>(st, dst); break;
                 default: load_a.template operator()<int(sizeof(T))>(st, dst); break;
             }
+        }
+        if (gather_fast) {
+            switch (int(sizeof(T)) << p.lvb) {
+                case 16: load_gather.template operator()<16>(st, dst + p.a_stage); break;
+                case 8: load_gather.template operator()<8>(st, dst + p.a_stage); break;
+                default: load_gather.template operator()<int(sizeof(T))>(st, dst + p.a_stage); break;
+            }
+            return;
         }
         switch (int(sizeof(T)) << p.lvb) {
             case 16: load_b.template operator()<16>(st, dst + p.a_stage); break;
