@@ -147,6 +147,8 @@ class ShardBackend final : public MeasurementBackend {
     std::string name() const override { return real_.name(); }
     double measure(const GemmInput& in, const GemmTuning& t) override { return record(mine() ? real_.measure(in, t) : -1.0); }
     double measure(const ConvInput& in, const ConvTuning& t) override { return record(mine() ? real_.measure(in, t) : -1.0); }
+    bool accepts(const GemmInput& in, const GemmTuning& t) const override { return real_.accepts(in, t); }
+    bool accepts(const ConvInput& in, const ConvTuning& t) const override { return real_.accepts(in, t); }
     std::vector<double> values;
 
   private:
@@ -161,10 +163,15 @@ class ShardBackend final : public MeasurementBackend {
 
 class ReplayBackend final : public MeasurementBackend {
   public:
-    ReplayBackend(std::string name, const double* v, std::int64_t n) : name_(std::move(name)), v_(v), n_(n) {}
+    // `launch` (may be null): the backend whose launchability filter the
+    // shards ranked with, so the replay ranks the same candidates.
+    ReplayBackend(std::string name, const double* v, std::int64_t n, std::unique_ptr<MeasurementBackend> launch)
+        : name_(std::move(name)), v_(v), n_(n), launch_(std::move(launch)) {}
     std::string name() const override { return name_; }
     double measure(const GemmInput&, const GemmTuning&) override { return take(); }
     double measure(const ConvInput&, const ConvTuning&) override { return take(); }
+    bool accepts(const GemmInput& in, const GemmTuning& t) const override { return !launch_ || launch_->accepts(in, t); }
+    bool accepts(const ConvInput& in, const ConvTuning& t) const override { return !launch_ || launch_->accepts(in, t); }
 
   private:
     double take() {
@@ -174,7 +181,17 @@ class ReplayBackend final : public MeasurementBackend {
     std::string name_;
     const double* v_;
     std::int64_t n_, i_{0};
+    std::unique_ptr<MeasurementBackend> launch_;
 };
+
+// The launchability filter behind a replayed backend name ("b200" /
+// "b200-parity"; anything else accepts every legal tuple).
+std::unique_ptr<MeasurementBackend> replay_filter(const char* name, const HardwareDescriptor& hw) {
+    const std::string n = name ? name : "b200";
+    if (n == "b200") return make_backend(1, hw, nullptr);
+    if (n == "b200-parity") return make_backend(2, hw, nullptr);
+    return nullptr;
+}
 
 }  // namespace
 
@@ -594,7 +611,7 @@ int ktune_infer_gemm_replay(const ktune_hw* hw, const char* bounds_json, const c
     return guard([&] {
         need(gflops, "gflops");
         const HardwareDescriptor h = conv_hw(hw);
-        ReplayBackend rb(backend_name ? backend_name : "b200", gflops, n);
+        ReplayBackend rb(backend_name ? backend_name : "b200", gflops, n, replay_filter(backend_name, h));
         auto pred = make_predictor(model_json, h);
         last_text() = to_json_text(infer_gemm(*pred, conv_in(in), h, gemm_bounds(bounds_json), top_k, rb));
     });
@@ -606,7 +623,7 @@ int ktune_infer_conv_replay(const ktune_hw* hw, const char* bounds_json, const c
     return guard([&] {
         need(gflops, "gflops");
         const HardwareDescriptor h = conv_hw(hw);
-        ReplayBackend rb(backend_name ? backend_name : "b200", gflops, n);
+        ReplayBackend rb(backend_name ? backend_name : "b200", gflops, n, replay_filter(backend_name, h));
         auto pred = make_predictor(model_json, h);
         last_text() = to_json_text(infer_conv(*pred, conv_in(in), h, conv_bounds(bounds_json), top_k, rb));
     });

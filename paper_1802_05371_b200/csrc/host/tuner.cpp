@@ -681,13 +681,23 @@ Result infer_any(const Input& input, const HardwareDescriptor& hw, const Bounds&
                  MeasurementBackend& backend, Predict predict) {
     input.validate();
     if (top_k < 1) throw std::invalid_argument("top_k must be >= 1");
-    const std::vector<Tuning> legal = enumerate_legal(input, hw, bounds);
+    std::vector<Tuning> legal = enumerate_legal(input, hw, bounds);
     if (legal.empty()) throw std::runtime_error("no legal configuration for this input");
+    const auto legal_size = std::int64_t(legal.size());
+    // Rank only what the measuring backend can run (the reference's CPU
+    // executors run every legal tuple; the B200 families reject tuples
+    // outside their launch envelope with unsupported_error, which would
+    // otherwise abort the top-k re-measure).  legal_space_size stays the
+    // whole legal space.
+    legal.erase(std::remove_if(legal.begin(), legal.end(),
+                               [&](const Tuning& t) { return !backend.accepts(input, t); }),
+                legal.end());
+    if (legal.empty()) throw std::runtime_error("no legal configuration this backend can launch for this input");
     std::vector<double> pred;
     predict(legal, pred);
     Result r;
     r.input = input;
-    r.legal_space_size = std::int64_t(legal.size());
+    r.legal_space_size = legal_size;
     for (std::size_t idx : best_k(legal, pred, std::size_t(top_k))) r.top_k.push_back({legal[idx], pred[idx], 0.0});
     std::size_t best = 0;
     for (std::size_t i = 0; i < r.top_k.size(); ++i) {

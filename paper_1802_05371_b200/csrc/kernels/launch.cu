@@ -336,13 +336,28 @@ void bind_workspace(Plan& pl, void* ws, std::size_t ws_bytes) {
 // geometry does not; PARITY keeps the reference's k_g slices.
 // KTUNE_SIMT_NZ forces a slice count (measurement); KTUNE_SIMT_NO_BALANCE
 // keeps k_g.
+// The slice span is also chosen so every k_l group start of every slice
+// (the ragged last one included) is 16-byte aligned: a K whose k_g slices
+// start on 4-byte boundaries (ICA 32x32x60000 at k_g = 64: span 938) would
+// otherwise be read by scalar cp.async instead of vectors / TMA boxes.
 std::int64_t balanced_span(const GemmInput& in, const GemmTuning& t, int es) {
     if (t.k_g < 2 || std::getenv("KTUNE_SIMT_NO_BALANCE") != nullptr) return 0;
     const std::int64_t tiles = ceil_div(in.m, t.m_l) * ceil_div(in.n, t.n_l);
     const std::int64_t sms = device_sm_count();
     const std::int64_t vec = 16 / es;
-    auto span_of = [&](std::int64_t nz) { return ceil_div(ceil_div(in.k, nz), vec) * vec; };
+    const bool kc = !in.trans_a || in.trans_b;  // an operand contiguous along K
+    auto aligned = [&](std::int64_t span) {
+        return slice_gcd_span(in.k, span, int(ceil_div(in.k, span)), t.k_l) % vec == 0;
+    };
+    auto span_of = [&](std::int64_t nz) {
+        const std::int64_t s0 = ceil_div(ceil_div(in.k, nz), vec) * vec;
+        if (!kc || in.k % vec != 0) return s0;
+        for (std::int64_t s = s0; s < s0 + 64 * vec * t.k_l && s < in.k; s += vec)
+            if (aligned(s)) return s;
+        return s0;
+    };
     if (const char* e = std::getenv("KTUNE_SIMT_NZ")) return span_of(std::max<std::int64_t>(1, std::atoll(e)));
+    const bool own_aligned = !kc || in.k % vec != 0 || aligned(ceil_div(in.k, t.k_g));
     std::int64_t best_nz = t.k_g;
     const std::int64_t per_sm0 = ceil_div(tiles * t.k_g, sms);
     double best = double(per_sm0) / double(t.k_g);
@@ -356,7 +371,7 @@ std::int64_t balanced_span(const GemmInput& in, const GemmTuning& t, int es) {
             best_nz = real;
         }
     }
-    return best_nz == t.k_g ? 0 : span_of(best_nz);
+    return best_nz == t.k_g && own_aligned ? 0 : span_of(best_nz);
 }
 
 Plan gemm_plan(const GemmInput& in, const GemmTuning& t, const void* a = nullptr, const void* b = nullptr,

@@ -14,6 +14,13 @@ device-measured data instead of the synthetic analytical device).
 3. report per-shape ratios pick / best and the count within 95 %.
 
     python scripts/selection_quality.py [--samples 12000] [--random 600] [--out profiles/...json]
+    python scripts/selection_quality.py --dtype bf16 ...   # tensor-core family
+
+With --dtype bf16 the same loop runs on the tcgen05 family: the
+gemm_b200_tc bounds, the calibrated tensor-core sampler fixture, bf16 inputs
+(the gemm.v1 features encode only the element size, so the model is trained
+on -- and used for -- one dtype; SURVEY 7's dtype decision), and only
+tuples the family can launch are ranked, drawn and measured.
 """
 from __future__ import annotations
 
@@ -32,6 +39,14 @@ import paper_1802_05371_b200 as K  # noqa: E402
 from paper_1802_05371_b200 import pipeline as P  # noqa: E402
 
 
+def launchable(inp, row):
+    try:
+        K.gemm_launch_info(inp, K.GemmTuning(*map(int, row)), "fast")
+        return True
+    except K.KtuneError:
+        return False
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--samples", type=int, default=12000)
@@ -39,30 +54,42 @@ def main():
     ap.add_argument("--top-k", type=int, default=20)
     ap.add_argument("--epochs", type=int, default=200)
     ap.add_argument("--extra-shapes", type=int, default=13)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_selection_quality.json"))
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--out", default=None)
     a = ap.parse_args()
+    tc = a.dtype != "f32"
+    if a.out is None:
+        a.out = os.path.join(ROOT, "profiles", "r2_selection_quality_bf16.json" if tc else "r1_selection_quality.json")
     import torch
     torch.cuda.set_device(0)
     hw = K.HardwareDescriptor.b200()
-    bounds = open(os.path.join(K.FIXTURES, "bounds", "gemm_b200.json")).read()
-    table = P.gemm_shapes_from_table(os.path.join(K.FIXTURES, "shapes", "benchmarks.json"))
+    bounds = open(os.path.join(K.FIXTURES, "bounds", "gemm_b200_tc.json" if tc else "gemm_b200.json")).read()
+    table = P.gemm_shapes_from_table(os.path.join(K.FIXTURES, "shapes", "benchmarks.json"), a.dtype)
     t0 = time.perf_counter()
-    sampler = P.calibrate(K.GemmInput(512, 512, 512), hw, bounds, 100000, 11)
-    dist = P.GemmInputDistribution(shapes=table, fixed_fraction=0.25)
+    if tc:  # the calibrated tensor-core sampler (fixtures/samplers, `calibrate --dtype bf16 --seed 11`)
+        sampler = open(os.path.join(K.FIXTURES, "samplers", "gemm_b200_tc_bf16.json")).read()
+    else:
+        sampler = P.calibrate(K.GemmInput(512, 512, 512), hw, bounds, 100000, 11)
+    dist = P.GemmInputDistribution(shapes=table, fixed_fraction=0.25, dtype=a.dtype)
     csv, stats = P.generate_sharded(sampler, dist, hw, bounds, a.samples, 42, backend="b200")
     t_gen = time.perf_counter() - t0
     t1 = time.perf_counter()
     fit = P.train_mlp(csv, epochs=a.epochs, seed=7)
     t_fit = time.perf_counter() - t1
     # test shapes: the table + fresh draws of the training distribution
-    ins, _, _, _ = P.predraw(sampler, P.GemmInputDistribution(shapes=[], fixed_fraction=0.0), hw, bounds,
-                             a.extra_shapes, 2024)
+    ins, _, _, _ = P.predraw(sampler, P.GemmInputDistribution(shapes=[], fixed_fraction=0.0, dtype=a.dtype), hw,
+                             bounds, a.extra_shapes, 2024)
     shapes = [("table:" + str(i), s) for i, s in enumerate(table)] + \
              [("draw:" + str(i), s) for i, s in enumerate(P.as_inputs(ins))]
     rng = np.random.default_rng(0)
     rows = []
     for name, inp in shapes:
         space = K.enumerate_legal(inp, hw, bounds, as_array=True)
+        if tc:  # the random reference points: launchable, one per tensor-core-distinct key
+            from paper_1802_05371_b200.tuner import tc_gemm_key
+            _, first = np.unique(np.asarray([tc_gemm_key(r) for r in space]), axis=0, return_index=True)
+            space = space[np.sort(first)]
+            space = space[np.asarray([launchable(inp, r) for r in space], bool)]
         res_m = json.loads(P.infer(inp, hw, bounds, fit.model_json, top_k=a.top_k, backend="b200"))
         res_a = json.loads(P.infer(inp, hw, bounds, None, top_k=a.top_k, backend="b200"))
         pick = [rng.integers(len(space))] if len(space) else []
@@ -92,7 +119,8 @@ def main():
               flush=True)
     mr = np.array([r["mlp_ratio"] for r in rows])
     ar = np.array([r["analytical_ratio"] for r in rows])
-    out = {"format": "ktune-b200-selection-1",
+    out = {"format": "ktune-b200-selection-1", "dtype": a.dtype,
+           "family": "tcgen05 (gemm_b200_tc bounds)" if tc else "simt fp32 (gemm_b200 bounds)",
            "dataset": {"samples": a.samples, "backend": "b200 (device measured)", "seconds": t_gen,
                        "samples_per_s": a.samples / t_gen},
            "mlp": {"hidden": [32, 64, 32], "epochs": a.epochs, "best_val_mse_log": fit.best_val_mse,

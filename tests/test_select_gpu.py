@@ -46,3 +46,26 @@ def test_infer_sharded_single_rank_on_device(cuda):
     assert len(meas) == 6 and all(m > 0 for m in meas)
     best = max(range(6), key=lambda i: (meas[i], -i))
     assert r["chosen"] == r["top_k"][best]["tuning"]
+
+
+def _tc_bounds():
+    import os
+    return open(os.path.join(K.FIXTURES, "bounds", "gemm_b200_tc.json")).read()
+
+
+def test_infer_tensor_core_ranks_only_launchable(cuda):
+    """most legal tuples of the tensor-core space are outside the
+    tcgen05 launch envelope; infer ranks only tuples the backend accepts, so
+    the top-k re-measure never aborts on unsupported_error, and the sharded
+    replay ranks the same candidates (same JSON as the sequential infer)."""
+    hw = K.HardwareDescriptor.b200()
+    bounds = _tc_bounds()
+    inp = K.GemmInput(1024, 96, 2048, "bf16")
+    r = json.loads(P.infer(inp, hw, bounds, None, top_k=8, backend="b200"))
+    assert len(r["top_k"]) == 8 and all(c["measured_gflops"] > 0 for c in r["top_k"])
+    assert r["legal_space_size"] == len(K.enumerate_legal(inp, hw, bounds))
+    for c in r["top_k"]:
+        K.gemm_launch_info(inp, K.GemmTuning(*(c["tuning"][n] for n in K.GEMM_PARAMS)), "fast")
+    s = json.loads(P.infer_sharded(inp, hw, bounds, None, 8, backend="b200"))
+    assert [c["tuning"] for c in s["top_k"]] == [c["tuning"] for c in r["top_k"]]
+    assert s["chosen"] in [c["tuning"] for c in s["top_k"]]

@@ -63,3 +63,22 @@ def test_random_shapes_fast_tolerance(cuda):
         a, b = O.fill(100 + trial, inp.m * inp.k, inp.k * inp.n, dt, True)
         got = run_gemm(inp, t, a, b, "fast")
         assert O.max_rel_error(got, exact(inp, a, b)) < fast_bound(inp), (inp, t)
+
+
+@pytest.mark.parametrize("kl", [1, 2, 4])
+def test_unaligned_slices_realigned_for_tma(cuda, kl):
+    """ICA 32x32x60000 at k_g = 64: the reference's slices start every 938
+    columns (4-byte aligned), which no vector / TMA feed can read; FAST
+    re-slices K so every k_l group start is 16-byte aligned and the TMA feed
+    runs; PARITY keeps the reference's slices (cp.async, bit-exact)."""
+    inp = K.GemmInput(32, 32, 60000, "f32", False, True)
+    t = K.GemmTuning(4, 1, 32, 8, 32, 4, kl, 64)
+    fast = K.gemm_launch_info(inp, t, "fast")
+    assert fast["family"] == "simt-tma", fast
+    assert K.gemm_launch_info(inp, t, "parity")["grid"][2] == 64
+    a, b = O.fill(29, inp.m * inp.k, inp.k * inp.n, "f32", True)
+    got = run_gemm(inp, t, a, b, "fast")
+    assert O.max_rel_error(got, exact(inp, a, b)) < fast_bound(inp)
+    par = run_gemm(inp, t, a, b, "parity")
+    want = O.execute_gemm(inp.m, inp.n, inp.k, 0, 1, t.values(), a, b)
+    assert bitwise_equal(par, want), first_mismatch(par, want)
