@@ -9,7 +9,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import bench, paper_1802_05371_b200 as K
 dev = torch.device("cuda:0"); torch.cuda.set_device(0)
-stream = torch.cuda.current_stream()
+stream = torch.cuda.Stream()  # graph capture needs a non-default stream
 hw = K.HardwareDescriptor.b200()
 shape = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "32,32,60000").split(",")]
 ta, tb = (False, True) if len(sys.argv) <= 2 else (sys.argv[2][0] == "T", sys.argv[2][1] == "T")
@@ -27,7 +27,9 @@ for i in idx:
     t = K.GemmTuning(*map(int, space[i]))
     try:
         ms = bench.time_gemm(inp, t, sets, stream, steps=20)
-    except Exception:
+    except Exception as e:  # noqa: BLE001 -- outside the launch envelope
+        if not res and i == idx[0]:
+            print("first failure:", e, flush=True)
         continue
     res.append((ms, t.values(), K.gemm_launch_info(inp, t, "fast")["family"]))
 res.sort()
@@ -40,4 +42,16 @@ top.sort()
 flops = 2 * inp.m * inp.n * inp.k
 for ms, v, fam in top[:15]:
     print(f"{ms*1e3:8.2f} us {flops/ms/1e9:7.2f} TF {v} {fam}")
+if os.environ.get("NZ_PROBE"):
+    # slice-count probe of the fastest tuples (FAST re-slicing forced)
+    for ms, v, fam in top[:3]:
+        row = []
+        for nz in [int(x) for x in os.environ["NZ_PROBE"].split(",")]:
+            os.environ["KTUNE_SIMT_NZ"] = str(nz)
+            try:
+                row.append((nz, round(bench.time_gemm(inp, K.GemmTuning(*v), sets, stream, steps=200) * 1e3, 2)))
+            except Exception as e:  # noqa: BLE001
+                row.append((nz, str(e)[:40]))
+        os.environ.pop("KTUNE_SIMT_NZ")
+        print("nz probe", v, row, flush=True)
 json.dump([[ms, v, fam] for ms, v, fam in top], open(os.path.join(os.environ.get("OUT_DIR", "gpurun_out"), "sweep_%s.json" % "_".join(map(str, shape))), "w"))
