@@ -152,9 +152,12 @@ KTUNE_API int ktune_build_indirection_table(const ktune_conv_input* in, int64_t*
 /* Workspace for k_g / c_g partials (0 bytes when the reduction is not split
  * across the grid): a 1 MiB region of per-tile arrival counters, then the
  * partials of every slice; the slice that arrives last folds them in slice
- * order and resets its counter.  The counter region (the first 1 MiB) must be
- * zero before a workspace's first use -- allocate with cudaMemset 0 -- and
- * every launch leaves it zero.  One launch at a time per workspace. */
+ * order and resets its counter (FAST with >= 16 slices instead adds the
+ * partials into an accumulator in the upper half of the counter region with
+ * L2 reductions; the last arrival stores C and re-zeroes it).  The counter
+ * region (the first 1 MiB) must be zero before a workspace's first use --
+ * allocate with cudaMemset 0 -- and every launch leaves it zero.  One launch
+ * at a time per workspace. */
 /* Launch geometry the library would use for this input/tuning (no launch):
  * threads per block, dynamic shared memory, grid {x, y, z}, and the kernel
  * family ("simt", "simt-tma", "simt-generic", "tcgen05", "tcgen05-pair"),

@@ -19,6 +19,7 @@
 #include <random>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -309,7 +310,15 @@ unsigned long long next_token() {
     return x == 0 ? 1 : x;
 }
 
-void bind_workspace(Plan& pl, void* ws, std::size_t ws_bytes) {
+// FAST k_g merge by L2 reductions (simt_store_or_merge): from this many
+// slices on, when the accumulator fits the upper half of the zeroed counter
+// region (its lower half holds the per-tile counters).  Measured on B200:
+// the ordered fold's latency grows with nz / FB round trips (ICA 32x32x60000
+// at 128 slices: 44 us of a 60 us launch).  KTUNE_SIMT_FOLD=ordered|atomic
+// overrides (measurement).
+constexpr int kAtomicFoldMinSlices = 16;
+
+void bind_workspace(Plan& pl, void* ws, std::size_t ws_bytes, Mode mode = Mode::parity, int esize = 4) {
     if (pl.p.nz <= 1) return;
     if (ws == nullptr || ws_bytes < pl.ws_bytes)
         throw workspace_error("workspace of " + std::to_string(ws_bytes) + " bytes is smaller than the " +
@@ -317,6 +326,16 @@ void bind_workspace(Plan& pl, void* ws, std::size_t ws_bytes) {
     pl.p.flags = static_cast<unsigned long long*>(ws);
     pl.p.ws = static_cast<unsigned char*>(ws) + pl.counter_bytes;
     pl.p.token = next_token();
+    pl.p.acc = nullptr;
+    if (mode != Mode::fast) return;
+    const char* f = std::getenv("KTUNE_SIMT_FOLD");
+    const bool forced = f != nullptr && std::strcmp(f, "atomic") == 0;
+    const bool ordered = f != nullptr && std::strcmp(f, "ordered") == 0;
+    const std::size_t half = pl.counter_bytes / 2;
+    const std::size_t tiles = std::size_t(pl.col_tiles) * std::size_t(pl.row_tiles);
+    if (!ordered && (forced || pl.p.nz >= kAtomicFoldMinSlices) && tiles * sizeof(unsigned) <= half &&
+        std::size_t(pl.p.out_elems) * std::size_t(esize) <= half)
+        pl.p.acc = static_cast<unsigned char*>(ws) + half;
 }
 
 // Pointers are only used for vector-width alignment (nullptr = assume the
@@ -680,7 +699,7 @@ void gemm(const GemmInput& in, const GemmTuning& t, Mode mode, const void* a, co
         return;
     }
     Plan pl = gemm_plan(in, t, a, b, mode == Mode::fast);
-    bind_workspace(pl, ws, ws_bytes);
+    bind_workspace(pl, ws, ws_bytes, mode, dtype_size_bytes(in.dtype));
     pick(false, in.dtype, mode, pl);  // resolves pl.generic
     TmaLaunch tl = tma_geometry(in, pl, mode, a, b);
     if (tl.kernel != nullptr) launch_gemm_tma(in, pl, tl, a, b, c, stream);
@@ -695,7 +714,7 @@ void conv(const ConvInput& in, const ConvTuning& t, Mode mode, const void* image
         return;
     }
     Plan pl = conv_plan(in, t, images, filters);
-    bind_workspace(pl, ws, ws_bytes);
+    bind_workspace(pl, ws, ws_bytes, mode, dtype_size_bytes(in.dtype));
     if (in.dtype == Dtype::f32) launch_conv_t<float>(in, t, pl, mode, images, filters, outputs, stream);
     else launch_conv_t<double>(in, t, pl, mode, images, filters, outputs, stream);
 }

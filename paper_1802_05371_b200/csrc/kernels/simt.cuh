@@ -60,6 +60,7 @@ struct SimtParams {
     int fast_ld;                // affine problems: per-thread chunk state precomputed (see ChunkLd)
     int gather_ld;              // CONV: per-thread gather chunk state precomputed (see GatherLd)
     long long* dbg;             // optional timeline probe (KTUNE_SIMT_DEBUG): blocks x = 0, y in {0, 1}
+    void* acc;                  // FAST k_g merge by reduction: zeroed [out_elems] accumulator, or nullptr
 };
 
 // Timeline probe (debug builds of a measurement: KTUNE_SIMT_DEBUG = device
@@ -292,10 +293,25 @@ __device__ __forceinline__ void simt_store_or_merge(const Prob& prob, const Simt
             if (row < p.rows && oc >= 0) idx[e] = prob.out_index(row, oc);
         }
     }
-    if (owner)
+    // FAST with many slices (p.acc): every slice adds its partial into a
+    // zeroed accumulator with fire-and-forget L2 reductions; the last
+    // arriver reads the sums once, stores C and re-zeroes the accumulator.
+    // One L2 round trip instead of nz / FB; the summation order is the
+    // arrival order (FAST's contract: within 1e-5 of the reference, not
+    // bitwise reproducible).  PARITY never takes this path.
+    T* acc = nullptr;
+    if constexpr (!PARITY) acc = static_cast<T*>(p.acc);
+    if (acc != nullptr) {
+        if (owner)
+#pragma unroll
+            for (int e = 0; e < TILE; ++e)
+                if (e < n && idx[e] >= 0) atomicAdd(acc + idx[e], blk[e]);
+        __threadfence();
+    } else if (owner) {
 #pragma unroll
         for (int e = 0; e < TILE; ++e)
             if (e < n && idx[e] >= 0) __stcg(ws + std::int64_t(g) * p.out_elems + idx[e], blk[e]);
+    }
     __shared__ int s_last;
     // bar.sync orders every thread's partial stores before thread 0's
     // gpu-scope release (cumulative); its acquire half orders the folding
@@ -311,6 +327,15 @@ __device__ __forceinline__ void simt_store_or_merge(const Prob& prob, const Simt
     }
     __syncthreads();
     if (!s_last || !owner) return;
+    if (acc != nullptr) {
+#pragma unroll
+        for (int e = 0; e < TILE; ++e)
+            if (e < n && idx[e] >= 0) {
+                out[idx[e]] = __ldcg(acc + idx[e]);
+                __stcg(acc + idx[e], T(0));
+            }
+        return;
+    }
     // Batches of FB slices: up to 16 independent L2 loads in flight, then the
     // adds in slice order (the order is what parity fixes, not the loads).
     // Wider batches were measured slower: the kernel's register count is set

@@ -80,6 +80,13 @@ __device__ __forceinline__ float4 tma_lds128(unsigned addr) {
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
     return v;
 }
+// owned rows / cols contiguous along the non-reduction dimension
+// (tx * NS + j): an even count starts 8-byte aligned, one LDS.64 per pair
+__device__ __forceinline__ float2 tma_lds64(unsigned addr) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ float tma_lds32(unsigned addr) {
     float v;
     asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v) : "r"(addr));
@@ -328,6 +335,12 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 4 * 32 : 1024)
                                     const float4 v = tma_lds128(ap + unsigned(i * ES));
                                     av[i] = v.x; av[i + 1] = v.y; av[i + 2] = v.z; av[i + 3] = v.w;
                                 }
+                            } else if constexpr (MS_ * ES % 8 == 0) {
+#pragma unroll
+                                for (int i = 0; i < MS_; i += 2) {
+                                    const float2 v = tma_lds64(ap + unsigned(i * ES));
+                                    av[i] = v.x; av[i + 1] = v.y;
+                                }
                             } else {
 #pragma unroll
                                 for (int i = 0; i < MS_; ++i) av[i] = tma_lds32(ap + unsigned(i * ES));
@@ -343,6 +356,12 @@ __global__ void __launch_bounds__(NARROW ? kNarrowThreads + 4 * 32 : 1024)
                                 for (int j = 0; j < NS_; j += VK) {
                                     const float4 v = tma_lds128(bp + unsigned(j * ES));
                                     bv[j] = v.x; bv[j + 1] = v.y; bv[j + 2] = v.z; bv[j + 3] = v.w;
+                                }
+                            } else if constexpr (NS_ * ES % 8 == 0) {
+#pragma unroll
+                                for (int j = 0; j < NS_; j += 2) {
+                                    const float2 v = tma_lds64(bp + unsigned(j * ES));
+                                    bv[j] = v.x; bv[j + 1] = v.y;
                                 }
                             } else {
 #pragma unroll

@@ -82,3 +82,28 @@ def test_unaligned_slices_realigned_for_tma(cuda, kl):
     par = run_gemm(inp, t, a, b, "parity")
     want = O.execute_gemm(inp.m, inp.n, inp.k, 0, 1, t.values(), a, b)
     assert bitwise_equal(par, want), first_mismatch(par, want)
+
+
+@pytest.mark.parametrize("fold,nz", [("auto", 128), ("auto", 40), ("atomic", 4), ("ordered", 64)])
+def test_fast_merge_by_reduction(cuda, monkeypatch, fold, nz):
+    """FAST merges >= 16 k_g slices with L2 reductions into a zeroed
+    accumulator in the counter region; the last arriver stores C and
+    re-zeroes it, so back-to-back launches on the same workspace (and the
+    ordered fold afterwards) stay correct.  PARITY is never affected."""
+    monkeypatch.setenv("KTUNE_SIMT_NZ", str(nz))
+    if fold != "auto":
+        monkeypatch.setenv("KTUNE_SIMT_FOLD", fold)
+    inp = K.GemmInput(32, 32, 60000, "f32", False, True)
+    t = K.GemmTuning(4, 4, 32, 32, 32, 1, 1, 64)
+    a, b = O.fill(nz, inp.m * inp.k, inp.k * inp.n, "f32", True)
+    want = exact(inp, a, b)
+    for _ in range(3):
+        got = run_gemm(inp, t, a, b, "fast")
+        assert O.max_rel_error(got, want) < fast_bound(inp)
+    monkeypatch.setenv("KTUNE_SIMT_FOLD", "ordered")
+    got = run_gemm(inp, t, a, b, "fast")
+    assert O.max_rel_error(got, want) < fast_bound(inp)
+    monkeypatch.delenv("KTUNE_SIMT_NZ")
+    par = run_gemm(inp, t, a, b, "parity")
+    ref = O.execute_gemm(inp.m, inp.n, inp.k, 0, 1, t.values(), a, b)
+    assert bitwise_equal(par, ref), first_mismatch(par, ref)

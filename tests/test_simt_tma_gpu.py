@@ -61,7 +61,10 @@ def test_tma_feed_is_bitwise(cuda, case):
         want = O.execute_gemm(m, n, k, ta, tb, tv, a, b, "f32")
         assert bitwise_equal(got, want), (case, first_mismatch(got, want))
     fast, fast_cp = both_feeds(inp, t, a, b, mode="fast")
-    assert bitwise_equal(fast, fast_cp), (case, first_mismatch(fast, fast_cp))
+    if K.gemm_launch_info(inp, t, "fast")["grid"][2] < 16:
+        assert bitwise_equal(fast, fast_cp), (case, first_mismatch(fast, fast_cp))
+    else:  # FAST merges >= 16 slices by L2 reductions: arrival order, not bitwise
+        assert O.max_rel_error(fast, fast_cp.astype(np.float64)) < 1e-5, case
     rows = min(m, 64)
     if not ta:
         # FAST (FFMA) within the reference's 1e-5 (test_backends.cpp:142), or
