@@ -487,7 +487,34 @@ bool tma_enabled() {
 std::size_t round_up(std::size_t x, std::size_t a) { return (x + a - 1) / a * a; }
 
 // Geometry of the TMA variant, or kernel == nullptr when not eligible.
-TmaLaunch tma_geometry(const GemmInput& in, const Plan& pl, Mode mode, const void* a, const void* b) {
+TmaLaunch tma_geometry_at(const GemmInput& in, const Plan& pl, Mode mode, const void* a, const void* b);
+
+// Stage width: the tuple's u only sets how many reduction columns a stage
+// stages (w = max(u / k_l, k_s)); the summation order is fixed by k_s, k_l
+// and k_g alone (backends.cpp:252-325; oracle: "only the three reduction
+// splits affect the result"), so the TMA feed may stage several u-steps per
+// box without changing a bit of either mode's result.  Small u (the C1
+// LINPACK tuple: u = 8, 32-byte boxes) otherwise spends its time issuing
+// TMA boxes: widen to 128-byte rows while every group keeps >= 2 steps.
+// KTUNE_SIMT_WIDEN=0 keeps the tuple's width (measurement).
+TmaLaunch tma_geometry(const GemmInput& in, Plan& pl, Mode mode, const void* a, const void* b) {
+    const int w0 = pl.p.w, lw0 = pl.p.lw;
+    const char* e = std::getenv("KTUNE_SIMT_WIDEN");
+    if (!(e != nullptr && e[0] == '0') && in.dtype == Dtype::f32) {
+        const std::int64_t kl_span = ceil_div(pl.p.kg_span, pl.p.kl);
+        while (pl.p.w * 2 <= 32 && kl_span >= std::int64_t(pl.p.w) * 4) {
+            pl.p.w *= 2;
+            ++pl.p.lw;
+        }
+    }
+    TmaLaunch tl = tma_geometry_at(in, pl, mode, a, b);
+    if (tl.kernel != nullptr || pl.p.w == w0) return tl;
+    pl.p.w = w0;  // not eligible when widened: the tuple's width (cp.async keeps it too)
+    pl.p.lw = lw0;
+    return tma_geometry_at(in, pl, mode, a, b);
+}
+
+TmaLaunch tma_geometry_at(const GemmInput& in, const Plan& pl, Mode mode, const void* a, const void* b) {
     TmaLaunch tl;
     const auto& p = pl.p;
     if (!tma_enabled() || in.dtype != Dtype::f32 || pl.generic) return tl;

@@ -108,3 +108,27 @@ def test_tma_unaligned_falls_back_identically(cuda):
     got, cp = both_feeds(inp, t, a, b)
     want = O.execute_gemm(50, 30, 333, False, False, t.values(), a, b, "f32")
     assert bitwise_equal(got, want) and bitwise_equal(cp, want)
+
+
+@pytest.mark.parametrize("case", [
+    ((512, 512, 512, False, False), (2, 8, 32, 32, 8, 1, 1, 1)),    # C1 fixed tuple: u = 8 staged 32 wide
+    ((300, 40, 2001, True, True), (2, 2, 16, 16, 8, 4, 2, 4)),      # k_s = 4, k_l = 2, ragged
+    ((256, 64, 1024, False, True), (4, 2, 32, 16, 4, 2, 1, 2)),     # u = 4
+])
+def test_widened_stages_are_bitwise(cuda, monkeypatch, case):
+    """The TMA feed stages several u-steps per box (u does not enter the
+    summation order: only k_s, k_l and k_g do); PARITY stays bit-identical
+    to the reference with and without widening, FAST within tolerance."""
+    (m, n, k, ta, tb), tv = case
+    inp = K.GemmInput(m, n, k, "f32", ta, tb)
+    t = K.GemmTuning(*tv)
+    a, b = O.fill(sum(tv), m * k, k * n, "f32", True)
+    want = O.execute_gemm(m, n, k, ta, tb, tv, a, b, "f32")
+    for widen in ("1", "0"):
+        monkeypatch.setenv("KTUNE_SIMT_WIDEN", widen)
+        assert K.gemm_launch_info(inp, t, "parity")["family"] == "simt-tma", case
+        got = run_gemm(inp, t, a, b, "parity")
+        assert bitwise_equal(got, want), (case, widen, first_mismatch(got, want))
+        fast = run_gemm(inp, t, a, b, "fast")
+        assert O.max_rel_error(fast, O.naive_gemm(m, n, k, int(ta), int(tb), a.astype(np.float64),
+                                                  b.astype(np.float64), "f64")) < max(1e-5, 2e-8 * k)
