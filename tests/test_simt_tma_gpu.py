@@ -130,5 +130,8 @@ def test_widened_stages_are_bitwise(cuda, monkeypatch, case):
         got = run_gemm(inp, t, a, b, "parity")
         assert bitwise_equal(got, want), (case, widen, first_mismatch(got, want))
         fast = run_gemm(inp, t, a, b, "fast")
-        assert O.max_rel_error(fast, O.naive_gemm(m, n, k, int(ta), int(tb), a.astype(np.float64),
-                                                  b.astype(np.float64), "f64")) < max(1e-5, 2e-8 * k)
+        # FAST within 1e-5, or within 2x the reference executor's own
+        # rounding error on these signed inputs (as test_tma_feed_is_bitwise)
+        ref = O.naive_gemm(m, n, k, int(ta), int(tb), a.astype(np.float64), b.astype(np.float64), "f64")
+        own = O.max_rel_error(want, ref)
+        assert O.max_rel_error(fast, ref) < max(1e-5, 2 * own), (case, widen)
