@@ -112,7 +112,7 @@ def test_tma_unaligned_falls_back_identically(cuda):
 
 @pytest.mark.parametrize("case", [
     ((512, 512, 512, False, False), (2, 8, 32, 32, 8, 1, 1, 1)),    # C1 fixed tuple: u = 8 staged 32 wide
-    ((300, 40, 2001, True, True), (2, 2, 16, 16, 8, 4, 2, 4)),      # k_s = 4, k_l = 2, ragged
+    ((300, 40, 2048, True, True), (2, 2, 16, 16, 8, 4, 2, 4)),      # k_s = 4, k_l = 2, ragged rows
     ((256, 64, 1024, False, True), (4, 2, 32, 16, 4, 2, 1, 2)),     # u = 4
 ])
 def test_widened_stages_are_bitwise(cuda, monkeypatch, case):
