@@ -155,7 +155,8 @@ int device_sm_count() {
 Plan plan_simt(std::int64_t rows, std::int64_t red, std::int64_t out_elems, std::int64_t col_tiles, int ml, int nl,
                int ms, int ns, int ks, int kl, int kg, int u, int esize, bool arm, bool brm,
                const std::function<int(int w, std::int64_t span_gcd)>& pick_va,
-               const std::function<int(int w, std::int64_t span_gcd)>& pick_vb, std::int64_t span_override = 0) {
+               const std::function<int(int w, std::int64_t span_gcd)>& pick_vb, std::int64_t span_override = 0,
+               bool widen = false) {
     Plan pl;
     auto& p = pl.p;
     p.rows = rows;
@@ -170,10 +171,14 @@ Plan plan_simt(std::int64_t rows, std::int64_t red, std::int64_t out_elems, std:
     p.tm = ml / ms;
     p.tn = nl / ns;
     p.w = std::max(u / kl, ks);
+    p.kg_span = span_override > 0 ? span_override : ceil_div(red, kg);
+    if (widen) {  // see stage_widen_enabled()
+        const std::int64_t kl_span = ceil_div(p.kg_span, kl);
+        while (p.w * 2 * esize <= 128 && kl_span >= std::int64_t(p.w) * 4) p.w *= 2;
+    }
     p.lw = ilog2(p.w);
     p.lml = ilog2(ml);
     p.lnl = ilog2(nl);
-    p.kg_span = span_override > 0 ? span_override : ceil_div(red, kg);
     p.nz = int(ceil_div(red, p.kg_span));
     const std::int64_t span_gcd = slice_gcd_span(red, p.kg_span, p.nz, kl);
     const int va = pick_va(p.w, span_gcd), vb = pick_vb(p.w, span_gcd);
@@ -393,6 +398,32 @@ std::int64_t balanced_span(const GemmInput& in, const GemmTuning& t, int es) {
     return best_nz == t.k_g && own_aligned ? 0 : span_of(best_nz);
 }
 
+// Stage width: the tuple's u only sets how many reduction columns a stage
+// holds (w = max(u / k_l, k_s)); the summation order is fixed by k_s, k_l
+// and k_g (c_s, c_l, c_g) alone (backends.cpp:252-325, 331-444; oracle:
+// "only the three reduction splits affect the result"), so a stage may hold
+// several u-steps -- up to 128-byte rows while every group keeps >= 4 steps
+// -- without changing a bit of either mode's result: fewer block barriers
+// (cp.async) and TMA issues per byte.  The widened plan is used when it
+// keeps the precomputed loaders and fits shared memory, else the tuple's.
+// KTUNE_SIMT_WIDEN=0 keeps the tuple's width (measurement).
+bool stage_widen_enabled() {
+    const char* e = std::getenv("KTUNE_SIMT_WIDEN");
+    return !(e != nullptr && e[0] == '0');
+}
+
+template <class Make>
+Plan widened_plan(const Make& make) {
+    if (stage_widen_enabled()) {
+        try {
+            Plan pl = make(true);
+            if (pl.p.fast_ld) return pl;
+        } catch (const unsupported_error&) {
+        }
+    }
+    return make(false);
+}
+
 Plan gemm_plan(const GemmInput& in, const GemmTuning& t, const void* a = nullptr, const void* b = nullptr,
                bool balance = false) {
     in.validate();
@@ -410,19 +441,23 @@ Plan gemm_plan(const GemmInput& in, const GemmTuning& t, const void* a = nullptr
     auto vb = [&](int w, std::int64_t span_gcd) {
         return brm ? vec_width(es, {in.k, span_gcd}, {b}, w) : vec_width(es, {in.n}, {b}, t.n_l);
     };
-    Plan pl = plan_simt(in.m, in.k, in.m * in.n, ceil_div(in.n, t.n_l), t.m_l, t.n_l, t.m_s, t.n_s, t.k_s, t.k_l,
-                        t.k_g, t.u, es, arm, brm, va, vb, balance ? balanced_span(in, t, es) : 0);
-    // Precomputed chunk loader: every thread's chunks fit ktune_dev::kChunkMax
-    // and every operand offset fits in 32 bits.
-    auto chunks = [&](int lrows, int lv) {
-        const std::int64_t total = std::int64_t(pl.p.kl) << (lrows + pl.p.lw - lv);
-        return ceil_div(total, pl.threads);
+    const std::int64_t span = balance ? balanced_span(in, t, es) : 0;
+    auto make = [&](bool widen) {
+        Plan pl = plan_simt(in.m, in.k, in.m * in.n, ceil_div(in.n, t.n_l), t.m_l, t.n_l, t.m_s, t.n_s, t.k_s,
+                            t.k_l, t.k_g, t.u, es, arm, brm, va, vb, span, widen);
+        // Precomputed chunk loader: every thread's chunks fit ktune_dev::kChunkMax
+        // and every operand offset fits in 32 bits.
+        auto chunks = [&](int lrows, int lv) {
+            const std::int64_t total = std::int64_t(pl.p.kl) << (lrows + pl.p.lw - lv);
+            return ceil_div(total, pl.threads);
+        };
+        const std::int64_t lim = std::int64_t(1) << 31;
+        pl.p.fast_ld = chunks(pl.p.lml, pl.p.lva) <= ktune_dev::kChunkMax &&
+                       chunks(pl.p.lnl, pl.p.lvb) <= ktune_dev::kChunkMax && in.m * in.k < lim &&
+                       in.k * in.n < lim && in.k + t.u < lim;
+        return pl;
     };
-    const std::int64_t lim = std::int64_t(1) << 31;
-    pl.p.fast_ld = chunks(pl.p.lml, pl.p.lva) <= ktune_dev::kChunkMax &&
-                   chunks(pl.p.lnl, pl.p.lvb) <= ktune_dev::kChunkMax && in.m * in.k < lim && in.k * in.n < lim &&
-                   in.k + t.u < lim;
-    return pl;
+    return widened_plan(make);
 }
 
 Plan conv_plan(const ConvInput& in, const ConvTuning& t, const void* img = nullptr, const void* flt = nullptr) {
@@ -442,16 +477,19 @@ Plan conv_plan(const ConvInput& in, const ConvTuning& t, const void* img = nullp
     auto va = [&](int, std::int64_t) { return vec_width(es, {in.k_filters}, {flt}, t.k_l); };
     // gather chunks must be whole n-runs: n_l and N multiples of the width
     auto vb = [&](int, std::int64_t) { return vec_width(es, {in.n_batch}, {img}, t.n_l); };
-    Plan pl = plan_simt(in.k_filters, in.c * in.r * in.s, in.k_filters * in.p * in.q * in.n_batch, col_tiles, t.k_l,
-                        t.p_l * t.q_l * t.n_l, t.k_s, t.p_s * t.q_s * t.n_s, t.c_s, t.c_l, t.c_g, t.u, es, false, false,
-                        va, vb);
-    // Precomputed chunk state for the filter operand (affine in the
-    // reduction index); the image gather keeps the tap decomposition.
-    const std::int64_t a_total = std::int64_t(pl.p.kl) << (pl.p.lml + pl.p.lw - pl.p.lva);
-    pl.p.fast_ld = ceil_div(a_total, pl.threads) <= ktune_dev::kChunkMax &&
-                   in.c * in.r * in.s * in.k_filters < (std::int64_t(1) << 31);
-    pl.p.gather_ld = std::getenv("KTUNE_SIMT_NO_GATHER") == nullptr ? 1 : 0;
-    return pl;
+    auto make = [&](bool widen) {
+        Plan pl = plan_simt(in.k_filters, in.c * in.r * in.s, in.k_filters * in.p * in.q * in.n_batch, col_tiles,
+                            t.k_l, t.p_l * t.q_l * t.n_l, t.k_s, t.p_s * t.q_s * t.n_s, t.c_s, t.c_l, t.c_g, t.u, es,
+                            false, false, va, vb, 0, widen);
+        // Precomputed chunk state for the filter operand (affine in the
+        // reduction index); the image gather keeps the tap decomposition.
+        const std::int64_t a_total = std::int64_t(pl.p.kl) << (pl.p.lml + pl.p.lw - pl.p.lva);
+        pl.p.fast_ld = ceil_div(a_total, pl.threads) <= ktune_dev::kChunkMax &&
+                       in.c * in.r * in.s * in.k_filters < (std::int64_t(1) << 31);
+        pl.p.gather_ld = std::getenv("KTUNE_SIMT_NO_GATHER") == nullptr ? 1 : 0;
+        return pl;
+    };
+    return widened_plan(make);
 }
 
 // ---- K1t: the TMA-fed variant (simt_tma.cuh) ------------------------------

@@ -107,3 +107,25 @@ def test_host_entry_and_validation(cuda):
     g = K.measure(K.ConvInput(16, 24, 240, 32, 16, 3, 3), K.ConvTuning(2, 1, 1, 1, 8, 1, 4, 2, 1, 1, 1, 8),
                   K.HardwareDescriptor())
     assert g > 0
+
+
+@pytest.mark.parametrize("widen", ["1", "0"])
+def test_widened_stages_conv_and_cp_async_gemm(cuda, monkeypatch, widen):
+    """Stages holding several u-steps (launch.cu widened_plan) leave the
+    summation order alone: the bench's fp32 ResNet conv pick and a cp.async
+    GEMM stay bit-identical to the reference with and without widening."""
+    monkeypatch.setenv("KTUNE_SIMT_WIDEN", widen)
+    cin = K.ConvInput(8, 14, 14, 32, 16, 3, 3)
+    ct = K.ConvTuning(8, 1, 2, 1, 32, 2, 2, 8, 16, 1, 1, 4)
+    ni, nf, _ = cin.sizes()
+    img, flt = O.fill(5, ni, nf, "f32")
+    got = run_conv(cin, ct, img, flt, "parity")
+    want = O.execute_conv([8, 14, 14, 32, 16, 3, 3], ct.values(), img, flt)
+    assert bitwise_equal(got, want), first_mismatch(got, want)
+    monkeypatch.setenv("KTUNE_SIMT_TMA", "0")
+    inp = K.GemmInput(200, 72, 1500, "f32", True, False)
+    t = K.GemmTuning(2, 2, 32, 16, 8, 2, 2, 2)
+    a, b = O.fill(9, inp.m * inp.k, inp.k * inp.n, "f32")
+    got = run_gemm(inp, t, a, b, "parity")
+    want = O.execute_gemm(inp.m, inp.n, inp.k, 1, 0, t.values(), a, b)
+    assert bitwise_equal(got, want), first_mismatch(got, want)
