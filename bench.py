@@ -670,9 +670,9 @@ def other_configs(stream, dev):
                      "layout": "CHWN/CRSK/KPQN (reference layouts, valid mode)",
                      "cudnn_tflops_nchw": cin.flops / cud / 1e9, "cudnn_tflops_nhwc": cin.flops / cud_cl / 1e9,
                      "ratio_vs_cudnn": min(cud, cud_cl) / ms, "rotating_sets": n_sets}
-        if name in ("conv_resnet56_bf16", "conv_resnet56_f32"):
-            res[name]["cpu_baseline"] = cpu_conv_tflops([cin.n_batch, cin.p, cin.q, cin.k_filters, cin.c, cin.r,
-                                                         cin.s], (1, 1, 1, 2, 16, 2, 2, 8, 8, 1, 1, 1))
+        # the reference executor beside every conv config (f32, host cores)
+        res[name]["cpu_baseline"] = cpu_conv_tflops([cin.n_batch, cin.p, cin.q, cin.k_filters, cin.c, cin.r, cin.s],
+                                                    (1, 1, 1, 2, 16, 2, 2, 8, 8, 1, 1, 1))
         del sets, xs, xs_cl
         torch.cuda.empty_cache()
 
