@@ -611,12 +611,13 @@ TmaLaunch tma_geometry_at(const GemmInput& in, const Plan& pl, Mode mode, const 
     {
         const std::int64_t blocks_total = std::int64_t(pl.col_tiles) * pl.row_tiles * p.nz;
         const std::int64_t per_sm = std::max<std::int64_t>(1, ceil_div(blocks_total, device_sm_count()));
-        // measured (bench protocol): extra producers never paid for the SIMT
-        // tiles of the benchmark shapes (2560x16x2560: 4-5 blocks/SM; 512^3:
-        // 2 blocks/SM, 9.4 -> 7.0 TFLOP/s with 2), so one unless asked for
-        (void)per_sm;
-        (void)boxes_per_step;
-        g.n_producers = 1;
+        // measured (bench protocol): with stages widened to 128-byte rows
+        // (tma_geometry) a second producer pays wherever a block shares its
+        // SM with at most two others -- 2560x16x2560 at 2 blocks/SM 15.98 ->
+        // 15.14 us, ICA 32x32x60000 17.8 -> 15.1 us, 1024^3 77.7 -> 69.6 us;
+        // a third was slower (15.5 us).  At 4-5 blocks per SM their own
+        // producers already overlap and the extra warps cost residency.
+        g.n_producers = (per_sm <= 3 && boxes_per_step >= 2) ? 2 : 1;
     }
     if (const char* e = std::getenv("KTUNE_SIMT_PRODUCERS")) g.n_producers = std::clamp(std::atoi(e), 1, 4);
     tl.threads = (g.producer_warp + g.n_producers) * 32;
