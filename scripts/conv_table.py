@@ -3,11 +3,12 @@ BASELINE configs[2]) on the B200: bf16 implicit-GEMM convolution on tcgen05,
 tuned per shape over the launchable tensor-core conv space (screened by cold
 single launches, top candidates re-timed back-to-back over rotating operand
 sets > 2x L2, CUDA-graph replay -- bench.py's protocol), against cuDNN (bf16,
-NCHW, its algorithm choice) under the same protocol.  Shapes outside the
+its algorithm choice; timed in NCHW and channels_last, the ratio is against
+the faster) under the same protocol.  Shapes outside the
 tensor-core envelope (batch not a multiple of 8, ...) are listed with the
 reason.  Valid-mode convolution, reference layouts CHWN / CRSK / KPQN.
 
-    python scripts/conv_table.py [--out profiles/r1_conv_table.json]
+    python scripts/conv_table.py [--out profiles/r2_conv_table.json]
 """
 from __future__ import annotations
 
@@ -29,7 +30,7 @@ from paper_1802_05371_b200.tuner import select_conv, tc_conv_key, tc_conv_launch
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--candidates", type=int, default=200)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_conv_table.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r2_conv_table.json"))
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -49,8 +50,14 @@ def main():
                  torch.empty(no, device=dev)) for _ in range(n_sets)]
         xs = [x[0].view(c, cin.h(), cin.w(), n).permute(3, 0, 1, 2).contiguous() for x in sets]
         w = sets[0][1].view(c, r, s, k).permute(3, 0, 1, 2).contiguous()
-        cud = time_torch(lambda i: torch.nn.functional.conv2d(xs[i], w), n_sets, st)
+        cud_nchw = time_torch(lambda i: torch.nn.functional.conv2d(xs[i], w), n_sets, st)
+        xs_cl = [x.contiguous(memory_format=torch.channels_last) for x in xs]
+        w_cl = w.contiguous(memory_format=torch.channels_last)
+        cud_cl = time_torch(lambda i: torch.nn.functional.conv2d(xs_cl[i], w_cl), n_sets, st)
+        cud = min(cud_nchw, cud_cl)
         row["cudnn_tflops"] = cin.flops / cud / 1e9
+        row["cudnn_tflops_nchw"] = cin.flops / cud_nchw / 1e9
+        row["cudnn_tflops_nhwc"] = cin.flops / cud_cl / 1e9
         try:
             sel = select_conv(cin, hw, bounds, candidates=a.candidates, top_k=6, key=tc_conv_key,
                               accept=tc_conv_launchable(cin))
@@ -73,7 +80,7 @@ def main():
         rows.append(row)
         print(name, {k_: (round(v, 2) if isinstance(v, float) else v) for k_, v in row.items()
                      if k_ in ("tflops", "cudnn_tflops", "ratio_vs_cudnn", "unsupported")}, flush=True)
-        del sets, xs
+        del sets, xs, xs_cl
         torch.cuda.empty_cache()
     ok = [r_ for r_ in rows if r_.get("family")]
     out = {"format": "ktune-b200-conv-table-1", "dtype": "bf16 in, fp32 out",
